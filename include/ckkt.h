@@ -1,0 +1,168 @@
+/* ckkt — condensed-KKT Newton-step solver for sm_100a (B200).
+ *
+ * C ABI of the per-iteration hot path of arXiv 2403.15913 (§IV-§V):
+ * one interior-point iteration needs the Newton step d solving
+ *
+ *     K_aug d = -r                                (Eq. kkt:augmented)
+ *
+ *           [ W_eff  0    G^T  H^T ]        r = (r1, r2, r3, r4)
+ *   K_aug = [ 0      D_s  0    I   ]        d = (dx, ds, dy, dz)
+ *           [ G      0    0    0   ]
+ *           [ H      I    0    0   ]        W_eff = W + diag(Sigma_x) + delta_x I  (reading R3)
+ *
+ * The library condenses K_aug into K_gamma = W_eff + H^T D_s H + gamma G^T G
+ * (P:310), factorizes it with a supernodal Cholesky on a pattern fixed at
+ * setup, and obtains d by
+ *   - CKKT_LIFTED  (m_e == 0): K dx = -r1 - H^T(D_s r4 - r2)   (Eq. liftedkkt)
+ *   - CKKT_HYKKT  : CG on S_gamma dy = r3 - G K_gamma^{-1} r_gamma (Eq. schurcomp),
+ *                   K_gamma dx = -r_gamma - G^T dy (reading R2 of P:394)
+ * followed by ds = -r4 - H dx, dz = -r2 - D_s ds and Richardson
+ * refinement on K_aug (reading R7).  Readings R* are in DESIGN.md §2.
+ *
+ * Conventions
+ *  - Indices are 0-based int32.  Matrices: W lower-triangular COO (row >= col,
+ *    duplicates are summed); G (m_e x n) and H (m_i x n) in CSR with strictly
+ *    increasing column indices per row.
+ *  - Pattern arrays are HOST memory, read during ckkt_setup only (copied).
+ *  - Value / rhs / result arrays passed to ckkt_refactor and ckkt_solve are
+ *    caller-owned DEVICE pointers to contiguous FP64 (or int32) data, batch-major:
+ *    instance b of a [B, len] array starts at ptr + b*len.
+ *  - All device work is enqueued on the caller's stream (options.stream); calls
+ *    return after enqueueing unless stated otherwise.  The library allocates all
+ *    its device memory in ckkt_setup and never in refactor/solve (fixed
+ *    pattern).
+ *  - Errors are return codes; nothing is thrown across the ABI.  A context is
+ *    used by one host thread at a time.
+ */
+#ifndef CKKT_H
+#define CKKT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ckkt_ctx ckkt_ctx;
+
+typedef enum {
+  CKKT_OK = 0,
+  CKKT_NOT_PD = 1,               /* Cholesky breakdown: wrong inertia. A result, not a failure. */
+  CKKT_CG_NO_CONVERGENCE = 2,    /* CG hit cg_maxit; the last iterate is returned */
+  CKKT_REFINE_NOT_CONVERGED = 3, /* refinement stopped above ref_tol; the best iterate is returned */
+  CKKT_PATTERN_ERROR = 4,        /* malformed pattern (index out of range, unsorted CSR, ...) */
+  CKKT_INVALID_ARG = 5,
+  CKKT_CUDA_ERROR = 6,
+  CKKT_OUT_OF_MEMORY = 7
+} ckkt_status;
+
+enum { CKKT_LIFTED = 0, CKKT_HYKKT = 1 };
+
+typedef struct {
+  int32_t n;                   /* number of primal variables x */
+  int32_t m_e;                 /* equality rows (G); must be 0 for CKKT_LIFTED */
+  int32_t m_i;                 /* inequality / relaxed rows (H), each with one slack */
+  int64_t w_nnz;               /* entries of W (lower COO) */
+  const int32_t *w_row, *w_col;
+  const int32_t *g_rowptr;     /* [m_e+1] (may be NULL when m_e == 0) */
+  const int32_t *g_col;        /* [g_rowptr[m_e]] */
+  const int32_t *h_rowptr;     /* [m_i+1] (may be NULL when m_i == 0) */
+  const int32_t *h_col;
+} ckkt_pattern;
+
+typedef struct {
+  int32_t strategy;            /* CKKT_LIFTED or CKKT_HYKKT */
+  double gamma;                /* HyKKT augmentation, default 1e7; ignored by Lifted */
+  double cg_rtol;              /* CG stop ||r_k||_2 <= cg_rtol ||b||_2, default 1e-10 (reading R6) */
+  int32_t cg_maxit;            /* default 200 */
+  double ref_tol;              /* refinement stop on the componentwise backward error, default 1e-14 (R7) */
+  int32_t ref_maxit;           /* default 10; 0 = no refinement */
+  int32_t batch;               /* B >= 1 independent instances sharing the pattern */
+  int32_t leaf;                /* nested-dissection leaf size, default 64 */
+  const int32_t *perm;         /* optional host [n] caller ordering (new -> old); NULL = built-in ND */
+  int32_t device;              /* CUDA device ordinal; -1 = host-only analysis (no device resources) */
+  void *stream;                /* cudaStream_t owned by the caller; NULL = legacy default stream */
+} ckkt_options;
+
+typedef struct {
+  int32_t status;              /* ckkt_status of this instance */
+  int32_t k_cg;                /* CG iterations of the unrefined solve (HyKKT) */
+  int32_t k_cg_total;          /* CG iterations summed over refinement passes */
+  int32_t n_ref;               /* Richardson corrections applied */
+  double rel_res;              /* componentwise backward error of the returned step (R7) */
+  double rel_res_unrefined;    /* same, before refinement */
+  double res_inf;              /* ||K_aug d + r||_inf of the returned step */
+} ckkt_info;
+
+typedef struct {
+  int32_t n, m_e, m_i, batch;
+  int64_t nnz_k;               /* lower-triangular entries of the K pattern (incl. diagonal) */
+  int64_t nnz_l;               /* entries of the exact L pattern (incl. diagonal), R11 */
+  int64_t l_storage;           /* doubles of supernodal factor storage per instance */
+  int32_t n_supernodes;
+  int32_t n_levels;            /* supernodal elimination-tree levels */
+  double flops_factor;         /* sum over columns of colcount^2 (algorithmic factor flops) */
+  int64_t device_bytes;        /* device memory owned by the context */
+} ckkt_sizes;
+
+/* Fill *opt with the defaults listed above (strategy HyKKT, batch 1, device 0). */
+void ckkt_default_options(ckkt_options *opt);
+
+/* Symbolic setup, once per pattern: K pattern = W ∪ G^T G ∪ H^T H ∪ diag,
+ * fill-reducing ordering, elimination tree, column counts, L pattern, supernodes,
+ * condensation maps; then device allocation and upload (unless device == -1).
+ * Returns CKKT_PATTERN_ERROR / CKKT_INVALID_ARG / CKKT_OUT_OF_MEMORY / CKKT_CUDA_ERROR. */
+ckkt_status ckkt_setup(const ckkt_pattern *pattern, const ckkt_options *opt, ckkt_ctx **out);
+
+/* Sizes of the analysis (host call, no synchronisation). */
+ckkt_status ckkt_get_sizes(const ckkt_ctx *ctx, ckkt_sizes *sizes);
+
+/* Copy the exact symbolic arrays (host memory, for bit-exact checks, R8/R11):
+ * perm[n] (new -> old), parent[n] (elimination tree of P K P^T, -1 = root),
+ * colcount[n], l_colptr[n+1] and l_rowind[nnz_l] (rows ascending, diagonal first).
+ * Any pointer may be NULL to skip that array. */
+ckkt_status ckkt_export_symbolic(const ckkt_ctx *ctx, int32_t *perm, int32_t *parent, int32_t *colcount,
+                                 int64_t *l_colptr, int32_t *l_rowind);
+
+/* Numeric refactorization of K_gamma from the values of one IPM iterate.
+ *   w_val [B, w_nnz], g_val [B, nnz(G)], h_val [B, nnz(H)], sigma_x [B, n], d_s [B, m_i] (> 0),
+ *   delta_x [B]  -- device FP64 (g_val/h_val/d_s may be NULL when the block is empty;
+ *   delta_x may be NULL = 0).
+ *   not_pd [B] (device int32, may be NULL): set to 1 where some pivot is <= 0 or not finite;
+ *   min_bad_pivot [B] (device int32, may be NULL): smallest failing column in the internal
+ *   elimination order, -1 if none (reading R9).
+ * Asynchronous: the flags are valid once the stream reaches this point.
+ * Zero-copy: the value arrays are read again by ckkt_solve (condensed rhs, SpMVs with G/H,
+ * K_aug residual), so they must stay valid and unmodified until the last ckkt_solve that
+ * uses this factorization has completed on the stream. */
+ckkt_status ckkt_refactor(ckkt_ctx *ctx, const double *w_val, const double *g_val, const double *h_val,
+                          const double *sigma_x, const double *d_s, const double *delta_x,
+                          int32_t *not_pd, int32_t *min_bad_pivot);
+
+/* Newton step for the last refactorization: r1 [B,n], r2 [B,m_i], r3 [B,m_e], r4 [B,m_i] in;
+ * dx [B,n], ds [B,m_i], dy [B,m_e], dz [B,m_i] out (device FP64; empty blocks may be NULL).
+ * info: HOST array [B] or NULL.  With info != NULL the call synchronises the stream,
+ * fills info and returns the worst per-instance status (NOT_PD instances get NaN steps
+ * and status CKKT_NOT_PD).  With NULL the call may still synchronise for its
+ * convergence tests but does not report. */
+ckkt_status ckkt_solve(ckkt_ctx *ctx, const double *r1, const double *r2, const double *r3, const double *r4,
+                       double *dx, double *ds, double *dy, double *dz, ckkt_info *info);
+
+/* End-to-end iteration from HOST buffers (pinned recommended): copies the values and
+ * right-hand sides to the device, refactorizes, solves and copies the step back.
+ * Same array shapes as ckkt_refactor / ckkt_solve, all host pointers. Synchronous. */
+ckkt_status ckkt_iterate_host(ckkt_ctx *ctx, const double *w_val, const double *g_val, const double *h_val,
+                              const double *sigma_x, const double *d_s, const double *delta_x,
+                              const double *r1, const double *r2, const double *r3, const double *r4,
+                              double *dx, double *ds, double *dy, double *dz, int32_t *not_pd, ckkt_info *info);
+
+/* Number of CUDA kernel launches enqueued by this context since creation (telemetry). */
+int64_t ckkt_launch_count(const ckkt_ctx *ctx);
+
+void ckkt_destroy(ckkt_ctx *ctx);
+const char *ckkt_status_str(ckkt_status s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CKKT_H */

@@ -1,0 +1,227 @@
+"""Thin ctypes binding of include/ckkt.h (argument marshalling only).
+
+Every numerical step runs inside libckkt.so (CUDA kernels for sm_100a); this
+module converts numpy / torch arguments to pointers and back.  It never falls
+back to a CPU implementation: if the library or a CUDA device is missing the
+calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libckkt.so")
+
+CKKT_OK, CKKT_NOT_PD, CKKT_CG_NO_CONVERGENCE, CKKT_REFINE_NOT_CONVERGED = 0, 1, 2, 3
+CKKT_PATTERN_ERROR, CKKT_INVALID_ARG, CKKT_CUDA_ERROR, CKKT_OUT_OF_MEMORY = 4, 5, 6, 7
+CKKT_LIFTED, CKKT_HYKKT = 0, 1
+
+EXPORTED = ["ckkt_default_options", "ckkt_setup", "ckkt_get_sizes", "ckkt_export_symbolic", "ckkt_refactor",
+            "ckkt_solve", "ckkt_iterate_host", "ckkt_launch_count", "ckkt_destroy", "ckkt_status_str"]
+
+
+class ckkt_pattern(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("m_e", ctypes.c_int32), ("m_i", ctypes.c_int32),
+                ("w_nnz", ctypes.c_int64), ("w_row", ctypes.c_void_p), ("w_col", ctypes.c_void_p),
+                ("g_rowptr", ctypes.c_void_p), ("g_col", ctypes.c_void_p),
+                ("h_rowptr", ctypes.c_void_p), ("h_col", ctypes.c_void_p)]
+
+
+class ckkt_options(ctypes.Structure):
+    _fields_ = [("strategy", ctypes.c_int32), ("gamma", ctypes.c_double), ("cg_rtol", ctypes.c_double),
+                ("cg_maxit", ctypes.c_int32), ("ref_tol", ctypes.c_double), ("ref_maxit", ctypes.c_int32),
+                ("batch", ctypes.c_int32), ("leaf", ctypes.c_int32), ("perm", ctypes.c_void_p),
+                ("device", ctypes.c_int32), ("stream", ctypes.c_void_p)]
+
+
+class ckkt_info(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int32), ("k_cg", ctypes.c_int32), ("k_cg_total", ctypes.c_int32),
+                ("n_ref", ctypes.c_int32), ("rel_res", ctypes.c_double), ("rel_res_unrefined", ctypes.c_double),
+                ("res_inf", ctypes.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class ckkt_sizes(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("m_e", ctypes.c_int32), ("m_i", ctypes.c_int32), ("batch", ctypes.c_int32),
+                ("nnz_k", ctypes.c_int64), ("nnz_l", ctypes.c_int64), ("l_storage", ctypes.c_int64),
+                ("n_supernodes", ctypes.c_int32), ("n_levels", ctypes.c_int32), ("flops_factor", ctypes.c_double),
+                ("device_bytes", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_lib = None
+
+
+def lib():
+    """Load libckkt.so (built in-tree by __graft_entry__.build()); raises if missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} missing: run __graft_entry__.build() (no CPU fallback exists)")
+        L = ctypes.CDLL(LIB_PATH)
+        P = ctypes.c_void_p
+        L.ckkt_default_options.argtypes = [ctypes.POINTER(ckkt_options)]
+        L.ckkt_default_options.restype = None
+        L.ckkt_setup.argtypes = [ctypes.POINTER(ckkt_pattern), ctypes.POINTER(ckkt_options), ctypes.POINTER(P)]
+        L.ckkt_setup.restype = ctypes.c_int
+        L.ckkt_get_sizes.argtypes = [P, ctypes.POINTER(ckkt_sizes)]
+        L.ckkt_get_sizes.restype = ctypes.c_int
+        L.ckkt_export_symbolic.argtypes = [P, P, P, P, P, P]
+        L.ckkt_export_symbolic.restype = ctypes.c_int
+        L.ckkt_refactor.argtypes = [P, P, P, P, P, P, P, P, P]
+        L.ckkt_refactor.restype = ctypes.c_int
+        L.ckkt_solve.argtypes = [P, P, P, P, P, P, P, P, P, ctypes.POINTER(ckkt_info)]
+        L.ckkt_solve.restype = ctypes.c_int
+        L.ckkt_iterate_host.argtypes = [P] * 16 + [ctypes.POINTER(ckkt_info)]
+        L.ckkt_iterate_host.restype = ctypes.c_int
+        L.ckkt_launch_count.argtypes = [P]
+        L.ckkt_launch_count.restype = ctypes.c_int64
+        L.ckkt_destroy.argtypes = [P]
+        L.ckkt_destroy.restype = None
+        L.ckkt_status_str.argtypes = [ctypes.c_int]
+        L.ckkt_status_str.restype = ctypes.c_char_p
+        _lib = L
+    return _lib
+
+
+class CKKTError(RuntimeError):
+    def __init__(self, code, where):
+        super().__init__(f"{where}: {lib().ckkt_status_str(code).decode()} ({code})")
+        self.code = code
+
+
+def _np_ptr(a):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _dptr(t):
+    """Device pointer of a contiguous torch CUDA tensor (or None)."""
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("device pointer expected (torch CUDA tensor)")
+    if not t.is_contiguous():
+        raise ValueError("tensor must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _hptr(a):
+    """Host pointer of a numpy array or a CPU torch tensor (pinned or not)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        assert a.flags.c_contiguous
+        return a.ctypes.data_as(ctypes.c_void_p)
+    if a.is_cuda:
+        raise ValueError("host pointer expected")
+    return ctypes.c_void_p(a.data_ptr())
+
+
+def default_options(**kw) -> ckkt_options:
+    o = ckkt_options()
+    lib().ckkt_default_options(ctypes.byref(o))
+    for k, v in kw.items():
+        setattr(o, k, v)
+    return o
+
+
+class Context:
+    """Owns one ckkt_ctx.  Method names follow the C ABI (ckkt_<name>)."""
+
+    def __init__(self, n, m_e, m_i, w_row, w_col, g_rowptr=None, g_col=None, h_rowptr=None, h_col=None,
+                 perm=None, stream=None, **options):
+        L = lib()
+        self._keep = []
+
+        def arr(a):
+            if a is None:
+                return None
+            a = np.ascontiguousarray(a, dtype=np.int32)
+            self._keep.append(a)
+            return a
+
+        w_row, w_col = arr(w_row), arr(w_col)
+        g_rowptr, g_col, h_rowptr, h_col = arr(g_rowptr), arr(g_col), arr(h_rowptr), arr(h_col)
+        pat = ckkt_pattern(n=n, m_e=m_e, m_i=m_i, w_nnz=len(w_row), w_row=_np_ptr(w_row), w_col=_np_ptr(w_col),
+                           g_rowptr=_np_ptr(g_rowptr), g_col=_np_ptr(g_col), h_rowptr=_np_ptr(h_rowptr),
+                           h_col=_np_ptr(h_col))
+        opt = default_options(**options)
+        if perm is not None:
+            perm = arr(perm)
+            opt.perm = _np_ptr(perm)
+        if stream is not None:
+            opt.stream = ctypes.c_void_p(stream)
+        self.opt = opt
+        self.n, self.m_e, self.m_i, self.batch = n, m_e, m_i, opt.batch
+        h = ctypes.c_void_p()
+        rc = L.ckkt_setup(ctypes.byref(pat), ctypes.byref(opt), ctypes.byref(h))
+        if rc != CKKT_OK:
+            raise CKKTError(rc, "ckkt_setup")
+        self.h = h
+        self._keep = []
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().ckkt_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- host-side queries
+    def get_sizes(self) -> dict:
+        s = ckkt_sizes()
+        rc = lib().ckkt_get_sizes(self.h, ctypes.byref(s))
+        if rc:
+            raise CKKTError(rc, "ckkt_get_sizes")
+        return s.as_dict()
+
+    def export_symbolic(self, pattern: bool = True):
+        sz = self.get_sizes()
+        n = sz["n"]
+        perm = np.empty(n, np.int32)
+        parent = np.empty(n, np.int32)
+        cc = np.empty(n, np.int32)
+        Lp = np.empty(n + 1, np.int64) if pattern else None
+        Li = np.empty(sz["nnz_l"], np.int32) if pattern else None
+        rc = lib().ckkt_export_symbolic(self.h, _np_ptr(perm), _np_ptr(parent), _np_ptr(cc), _np_ptr(Lp), _np_ptr(Li))
+        if rc:
+            raise CKKTError(rc, "ckkt_export_symbolic")
+        return perm, parent, cc, Lp, Li
+
+    def launch_count(self) -> int:
+        return int(lib().ckkt_launch_count(self.h))
+
+    # ---- device calls (torch CUDA tensors, batch-major)
+    def refactor(self, w_val, g_val, h_val, sigma_x, d_s=None, delta_x=None, not_pd=None, min_bad_pivot=None):
+        rc = lib().ckkt_refactor(self.h, _dptr(w_val), _dptr(g_val), _dptr(h_val), _dptr(sigma_x), _dptr(d_s),
+                                 _dptr(delta_x), _dptr(not_pd), _dptr(min_bad_pivot))
+        if rc:
+            raise CKKTError(rc, "ckkt_refactor")
+
+    def solve(self, r1, r2, r3, r4, dx, ds, dy, dz, want_info: bool = True):
+        infos = (ckkt_info * self.batch)() if want_info else None
+        rc = lib().ckkt_solve(self.h, _dptr(r1), _dptr(r2), _dptr(r3), _dptr(r4), _dptr(dx), _dptr(ds), _dptr(dy),
+                              _dptr(dz), infos)
+        if rc in (CKKT_INVALID_ARG, CKKT_CUDA_ERROR, CKKT_OUT_OF_MEMORY, CKKT_PATTERN_ERROR):
+            raise CKKTError(rc, "ckkt_solve")
+        return rc, ([i.as_dict() for i in infos] if want_info else None)
+
+    def iterate_host(self, w_val, g_val, h_val, sigma_x, d_s, delta_x, r1, r2, r3, r4, dx, ds, dy, dz, not_pd=None):
+        infos = (ckkt_info * self.batch)()
+        rc = lib().ckkt_iterate_host(self.h, _hptr(w_val), _hptr(g_val), _hptr(h_val), _hptr(sigma_x), _hptr(d_s),
+                                     _hptr(delta_x), _hptr(r1), _hptr(r2), _hptr(r3), _hptr(r4), _hptr(dx), _hptr(ds),
+                                     _hptr(dy), _hptr(dz), _hptr(not_pd), infos)
+        if rc in (CKKT_INVALID_ARG, CKKT_CUDA_ERROR, CKKT_OUT_OF_MEMORY, CKKT_PATTERN_ERROR):
+            raise CKKTError(rc, "ckkt_iterate_host")
+        return rc, [i.as_dict() for i in infos]

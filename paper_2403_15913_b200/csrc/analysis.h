@@ -1,0 +1,72 @@
+// Host-side symbolic analysis of the condensed KKT pattern.
+// Independent of oracle/ (no shared code); the ordering follows DESIGN.md §5.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace ckkt {
+
+struct Pattern {
+  int n = 0, me = 0, mi = 0;
+  std::vector<int32_t> w_row, w_col;
+  std::vector<int32_t> g_rowptr, g_col, h_rowptr, h_col;
+};
+
+// Result of the analysis.  "spec" arrays are w.r.t. the exported ordering perm
+// (bit-exact contract); the "internal" arrays use perm2 = perm ∘ postorder,
+// which has the same fill and contiguous supernodes (reading R11).
+struct Analysis {
+  Pattern pat;
+  int n = 0;
+  // K pattern as sorted unique lower pairs (original indices): key = i * n + j, i >= j
+  std::vector<int64_t> kpairs;
+  // adjacency of K without self loops (original indices), lists ascending
+  std::vector<int32_t> xadj, adj;
+  // exported ordering and its symbolic results
+  std::vector<int32_t> perm, parent, colcount;
+  int64_t nnz_l = 0;
+  double flops = 0.0;  // sum colcount^2
+  // internal ordering
+  std::vector<int32_t> perm2, iperm2;
+  std::vector<int64_t> kp;      // internal lower CSC of P2 K P2^T: column pointers [n+1]
+  std::vector<int32_t> ki;      // row indices
+  std::vector<int32_t> parent2, colcount2;
+  // supernodes (internal order): columns [sfirst[s], sfirst[s+1])
+  int ns = 0;
+  std::vector<int32_t> sfirst, snode_of, sparent, slevel;
+  std::vector<int64_t> srowptr;  // row structure of s: srows[srowptr[s] .. srowptr[s+1])
+  std::vector<int32_t> srows;
+  std::vector<int64_t> pofs;     // panel offsets (column-major m_s x w_s), [ns+1]
+  int nlevels = 0;
+  std::vector<int32_t> level_ptr, level_list;  // supernodes grouped by level (bottom-up)
+  // left-looking update pairs d -> s: for s, entries upd_ptr[s] .. upd_ptr[s+1]
+  std::vector<int32_t> upd_ptr, upd_d, upd_p, upd_q;
+  std::vector<int64_t> upd_rel;  // offset of the relative row map (rows [p, m_d) of d in srows[s])
+  std::vector<int32_t> relmap;
+  // condensation: per internal K slot k (CSC order)
+  std::vector<int32_t> kmap;     // position inside the instance's panel storage
+  std::vector<int64_t> wt_ptr;   // W entries summed into slot k
+  std::vector<int32_t> wt_idx;
+  std::vector<int32_t> dslot;    // [n] slot of the diagonal of internal column j
+  std::vector<int64_t> jt_ptr;   // J^T D J product terms of slot k
+  std::vector<int32_t> jt_a, jt_b, jt_r;  // entry indices a, b (into g or h values) and row r
+                                          // (r < me: G row, weight gamma; else H row r-me, weight d_s)
+  // transposed J (by internal column j): entries of G and H in column perm2[j]
+  std::vector<int32_t> gt_ptr, gt_e, gt_r, ht_ptr, ht_e, ht_r;
+  // G, H column indices mapped to internal order
+  std::vector<int32_t> g_col2, h_col2;
+  // W entries mapped to internal order, for the residual SpMV (row2 >= col2 not guaranteed)
+  std::vector<int32_t> w_row2, w_col2;
+};
+
+// Returns "" on success, else an error message; code receives a ckkt_status value.
+std::string analyze(const Pattern& p, int leaf, const int32_t* user_perm, Analysis& A, int& code);
+
+// Exact L pattern for the exported ordering (computed on demand).
+void export_l_pattern(const Analysis& A, std::vector<int64_t>& Lp, std::vector<int32_t>& Li);
+
+// Nested-dissection ordering of DESIGN.md §5 (exposed for testing).
+std::vector<int32_t> nd_order(int n, const std::vector<int32_t>& xadj, const std::vector<int32_t>& adj, int leaf);
+
+}  // namespace ckkt

@@ -1,0 +1,1301 @@
+// ckkt: condensed-KKT Newton-step solver — CUDA kernels (sm_100a) and the C ABI of include/ckkt.h.
+//
+// Per-iteration path; every step runs in the kernels below:
+//   a1 k_condense        K_gamma values from W, Sigma_x, delta_x, J, D_s, gamma
+//   a2 k_rhs             r~ = r1 + H^T(D_s r4 - r2) [+ gamma G^T r3]
+//   a3 k_factor          supernodal left-looking Cholesky, level scheduled
+//   a4 k_fwd / k_bwd     supernodal triangular solves, level scheduled
+//   a5 CG kernels        matrix-free CG on S_gamma = G K^{-1} G^T
+//   a6/a7 k_recover      dx un-permutation, ds = -r4 - H dx, dz = -r2 - D_s ds
+//   a8 k_kaug_residual   rho = -r - K_aug d and componentwise backward error        (R7)
+//   a9 flags             NOT_PD / minimum failing pivot
+// All n-vectors on the device live in the internal elimination order (perm2).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/ckkt.h"
+#include "analysis.h"
+
+#define CK(x)                                         \
+  do {                                                \
+    cudaError_t e_ = (x);                             \
+    if (e_ != cudaSuccess) {                          \
+      last_cuda_error = e_;                           \
+      return CKKT_CUDA_ERROR;                         \
+    }                                                 \
+  } while (0)
+
+static thread_local cudaError_t last_cuda_error = cudaSuccess;
+
+namespace {
+
+constexpr int TPB = 256;
+
+inline unsigned nblk(int64_t n, int t = TPB) { return (unsigned)((n + t - 1) / t); }
+
+// ------------------------------------------------------------------------------------------
+// a1: condensation.  One thread per K slot of the internal lower CSC; the sum order is fixed
+// by the maps (W terms, diagonal, J^T D J product terms in row order).
+// ------------------------------------------------------------------------------------------
+__global__ void k_condense(int64_t nnzk, const int64_t* __restrict__ wt_ptr, const int32_t* __restrict__ wt_idx,
+                           const int64_t* __restrict__ jt_ptr, const int32_t* __restrict__ jt_a,
+                           const int32_t* __restrict__ jt_b, const int32_t* __restrict__ jt_r,
+                           const int32_t* __restrict__ kdiag, const double* __restrict__ w_val, int64_t w_nnz,
+                           const double* __restrict__ g_val, int64_t g_nnz, const double* __restrict__ h_val,
+                           int64_t h_nnz, const double* __restrict__ sigma, const double* __restrict__ d_s,
+                           const double* __restrict__ delta, double gamma, int n, int me, int mi,
+                           double* __restrict__ Kval) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (k >= nnzk) return;
+  const double* w = w_val + b * w_nnz;
+  const double* g = g_val + b * g_nnz;
+  const double* h = h_val + b * h_nnz;
+  double acc = 0.0;
+  for (int64_t t = wt_ptr[k]; t < wt_ptr[k + 1]; ++t) acc += w[wt_idx[t]];
+  const int dv = kdiag[k];
+  if (dv >= 0) acc += sigma[(int64_t)b * n + dv] + (delta ? delta[b] : 0.0);
+  for (int64_t t = jt_ptr[k]; t < jt_ptr[k + 1]; ++t) {
+    const int r = jt_r[t];
+    if (r < me) acc += gamma * (g[jt_a[t]] * g[jt_b[t]]);
+    else acc += d_s[(int64_t)b * mi + (r - me)] * (h[jt_a[t]] * h[jt_b[t]]);
+  }
+  Kval[b * nnzk + k] = acc;
+}
+
+struct SymDev {
+  const int32_t* sfirst;
+  const int64_t* srowptr;
+  const int32_t* srows;
+  const int64_t* pofs;
+  const int32_t* level_list;
+  const int32_t* upd_ptr;
+  const int32_t* upd_d;
+  const int32_t* upd_p;
+  const int32_t* upd_q;
+  const int64_t* upd_rel;
+  const int32_t* relmap;
+  const int64_t* kp;
+  const int32_t* kmap;
+  const int32_t* perm2;
+};
+
+// ------------------------------------------------------------------------------------------
+// a3: numeric factorization of the supernodes of one level (one CTA per supernode and instance).
+// Left-looking: the panel gathers the updates of every descendant d with rows in its columns,
+// then is factorized densely (Cholesky of the diagonal block + column scaling).
+// ------------------------------------------------------------------------------------------
+__global__ void k_factor(SymDev S, int lvl_off, double* __restrict__ L, int64_t Lsize,
+                         const double* __restrict__ Kval, int64_t nnzk, int* __restrict__ notpd,
+                         int* __restrict__ minpiv) {
+  const int s = S.level_list[lvl_off + blockIdx.x];
+  const int b = blockIdx.y;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  double* Lb = L + b * Lsize;
+  const double* Kb = Kval + b * nnzk;
+  const int f = S.sfirst[s], w = S.sfirst[s + 1] - f;
+  const int64_t r0 = S.srowptr[s];
+  const int m = (int)(S.srowptr[s + 1] - r0);
+  double* P = Lb + S.pofs[s];
+  for (int64_t i = tid; i < (int64_t)m * w; i += nt) P[i] = 0.0;
+  __syncthreads();
+  for (int64_t k = S.kp[f] + tid; k < S.kp[f + w]; k += nt) P[S.kmap[k]] = Kb[k];
+  __syncthreads();
+  for (int u = S.upd_ptr[s]; u < S.upd_ptr[s + 1]; ++u) {
+    const int d = S.upd_d[u], p = S.upd_p[u], q = S.upd_q[u];
+    const int32_t* rel = S.relmap + S.upd_rel[u];
+    const double* Pd = Lb + S.pofs[d];
+    const int md = (int)(S.srowptr[d + 1] - S.srowptr[d]);
+    const int wd = S.sfirst[d + 1] - S.sfirst[d];
+    const int32_t* rd = S.srows + S.srowptr[d];
+    const int nr = md - p, nc = q - p;
+    for (int e = tid; e < nr * nc; e += nt) {
+      const int i = e % nr, c = e / nr;
+      if (i < c) continue;
+      double t = 0.0;
+      for (int kk = 0; kk < wd; ++kk) t += Pd[p + i + (int64_t)kk * md] * Pd[p + c + (int64_t)kk * md];
+      P[rel[i] + (int64_t)(rd[p + c] - f) * m] -= t;
+    }
+    __syncthreads();
+  }
+  __shared__ double piv;
+  for (int j = 0; j < w; ++j) {
+    if (tid == 0) {
+      double dj = P[j + (int64_t)j * m];
+      if (!(dj > 0.0) || !isfinite(dj)) {
+        notpd[b] = 1;
+        atomicMin(&minpiv[b], f + j);
+        dj = nan("");
+      }
+      piv = sqrt(dj);
+      P[j + (int64_t)j * m] = piv;
+    }
+    __syncthreads();
+    const double pv = piv;
+    for (int i = j + 1 + tid; i < m; i += nt) P[i + (int64_t)j * m] /= pv;
+    __syncthreads();
+    const int nrest = w - j - 1;
+    for (int e = tid; e < nrest * m; e += nt) {
+      const int c = j + 1 + e / m, i = e % m;
+      if (i >= c) P[i + (int64_t)c * m] -= P[i + (int64_t)j * m] * P[c + (int64_t)j * m];
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// a4: forward substitution L y = x (in place, internal order) for the supernodes of one level.
+// ------------------------------------------------------------------------------------------
+__global__ void k_fwd(SymDev S, int lvl_off, const double* __restrict__ L, int64_t Lsize, double* __restrict__ X,
+                      int n, const int* __restrict__ skip) {
+  extern __shared__ double y[];
+  const int s = S.level_list[lvl_off + blockIdx.x];
+  const int b = blockIdx.y;
+  if (skip && skip[b]) return;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const double* Lb = L + b * Lsize;
+  double* x = X + (int64_t)b * n;
+  const int f = S.sfirst[s], w = S.sfirst[s + 1] - f;
+  const int m = (int)(S.srowptr[s + 1] - S.srowptr[s]);
+  const double* P = Lb + S.pofs[s];
+  for (int i = tid; i < w; i += nt) y[i] = x[f + i];
+  __syncthreads();
+  for (int u = S.upd_ptr[s]; u < S.upd_ptr[s + 1]; ++u) {
+    const int d = S.upd_d[u], p = S.upd_p[u], q = S.upd_q[u];
+    const double* Pd = Lb + S.pofs[d];
+    const int md = (int)(S.srowptr[d + 1] - S.srowptr[d]);
+    const int fd = S.sfirst[d], wd = S.sfirst[d + 1] - fd;
+    const int32_t* rd = S.srows + S.srowptr[d];
+    for (int c = p + tid; c < q; c += nt) {
+      double t = 0.0;
+      for (int kk = 0; kk < wd; ++kk) t += Pd[c + (int64_t)kk * md] * x[fd + kk];
+      y[rd[c] - f] -= t;
+    }
+    __syncthreads();
+  }
+  for (int j = 0; j < w; ++j) {
+    if (tid == 0) y[j] /= P[j + (int64_t)j * m];
+    __syncthreads();
+    const double yj = y[j];
+    for (int i = j + 1 + tid; i < w; i += nt) y[i] -= P[i + (int64_t)j * m] * yj;
+    __syncthreads();
+  }
+  for (int i = tid; i < w; i += nt) x[f + i] = y[i];
+}
+
+// backward substitution L^T x = y for the supernodes of one level (levels processed top-down)
+__global__ void k_bwd(SymDev S, int lvl_off, const double* __restrict__ L, int64_t Lsize, double* __restrict__ X,
+                      int n, const int* __restrict__ skip) {
+  extern __shared__ double y[];
+  __shared__ double red[TPB / 32];
+  const int s = S.level_list[lvl_off + blockIdx.x];
+  const int b = blockIdx.y;
+  if (skip && skip[b]) return;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const double* Lb = L + b * Lsize;
+  double* x = X + (int64_t)b * n;
+  const int f = S.sfirst[s], w = S.sfirst[s + 1] - f;
+  const int64_t r0 = S.srowptr[s];
+  const int m = (int)(S.srowptr[s + 1] - r0);
+  const double* P = Lb + S.pofs[s];
+  for (int c = tid; c < w; c += nt) {
+    double t = x[f + c];
+    for (int i = w; i < m; ++i) t -= P[i + (int64_t)c * m] * x[S.srows[r0 + i]];
+    y[c] = t;
+  }
+  __syncthreads();
+  for (int j = w - 1; j >= 0; --j) {
+    // y[j] = (y[j] - sum_{i>j} P[i,j] y[i]) / P[j,j]
+    double part = 0.0;
+    for (int i = j + 1 + tid; i < w; i += nt) part += P[i + (int64_t)j * m] * y[i];
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_down_sync(0xffffffffu, part, o);
+    if ((tid & 31) == 0) red[tid >> 5] = part;
+    __syncthreads();
+    if (tid == 0) {
+      double tsum = 0.0;
+      for (int k = 0; k < nt / 32; ++k) tsum += red[k];
+      y[j] = (y[j] - tsum) / P[j + (int64_t)j * m];
+    }
+    __syncthreads();
+  }
+  for (int i = tid; i < w; i += nt) x[f + i] = y[i];
+}
+
+__global__ void k_init_flags(int B, int* notpd, int* minpiv) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < B) { notpd[b] = 0; minpiv[b] = INT_MAX; }
+}
+
+__global__ void k_final_flags(int B, const int* notpd_in, const int* minpiv_in, const int32_t* perm2, int* notpd_out,
+                              int* minpiv_out) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  if (notpd_out) notpd_out[b] = notpd_in[b];
+  if (minpiv_out) minpiv_out[b] = (minpiv_in[b] == INT_MAX) ? -1 : perm2[minpiv_in[b]];
+}
+
+// ------------------------------------------------------------------------------------------
+// a2: condensed rhs in internal order:  out[j] = s1*r1[perm2 j] + sum_H h (D_s r4 - r2) + gamma sum_G g r3
+// (s1 = +1; r1 may be given in internal order when r1_internal != 0)
+// ------------------------------------------------------------------------------------------
+__global__ void k_rhs(int n, int me, int mi, const int32_t* __restrict__ perm2, const double* __restrict__ r1,
+                      int r1_internal, const double* __restrict__ r2, const double* __restrict__ r3,
+                      const double* __restrict__ r4, const int32_t* __restrict__ gt_ptr,
+                      const int32_t* __restrict__ gt_e, const int32_t* __restrict__ gt_r,
+                      const int32_t* __restrict__ ht_ptr, const int32_t* __restrict__ ht_e,
+                      const int32_t* __restrict__ ht_r, const double* __restrict__ g_val, int64_t g_nnz,
+                      const double* __restrict__ h_val, int64_t h_nnz, const double* __restrict__ d_s, double gamma,
+                      double* __restrict__ out, const int* __restrict__ skip) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (j >= n || (skip && skip[b])) return;
+  double acc = r1[(int64_t)b * n + (r1_internal ? j : perm2[j])];
+  const double* h = h_val + b * h_nnz;
+  for (int t = ht_ptr[j]; t < ht_ptr[j + 1]; ++t) {
+    const int r = ht_r[t];
+    const int64_t o = (int64_t)b * mi + r;
+    acc += h[ht_e[t]] * (d_s[o] * r4[o] - r2[o]);
+  }
+  if (me > 0 && gamma != 0.0) {
+    const double* g = g_val + b * g_nnz;
+    double sg = 0.0;
+    for (int t = gt_ptr[j]; t < gt_ptr[j + 1]; ++t) sg += g[gt_e[t]] * r3[(int64_t)b * me + gt_r[t]];
+    acc += gamma * sg;
+  }
+  out[(int64_t)b * n + j] = acc;
+}
+
+// y[j] = alpha * sum_{G entries in column j} g * v[row]   (+ beta * z[j] if z)
+__global__ void k_gt_spmv(int n, int me, const int32_t* __restrict__ gt_ptr, const int32_t* __restrict__ gt_e,
+                          const int32_t* __restrict__ gt_r, const double* __restrict__ g_val, int64_t g_nnz,
+                          const double* __restrict__ v, double alpha, const double* __restrict__ z, double beta,
+                          double* __restrict__ y, const int* __restrict__ skip) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (j >= n || (skip && skip[b])) return;
+  const double* g = g_val + b * g_nnz;
+  double acc = 0.0;
+  for (int t = gt_ptr[j]; t < gt_ptr[j + 1]; ++t) acc += g[gt_e[t]] * v[(int64_t)b * me + gt_r[t]];
+  double r = alpha * acc;
+  if (z) r += beta * z[(int64_t)b * n + j];
+  y[(int64_t)b * n + j] = r;
+}
+
+// y[r] = alpha * (G x)[r] + beta * z[r]
+__global__ void k_g_spmv(int me, int n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col2,
+                         const double* __restrict__ g_val, int64_t g_nnz, const double* __restrict__ x, double alpha,
+                         const double* __restrict__ z, double beta, double* __restrict__ y,
+                         const int* __restrict__ skip) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (r >= me || (skip && skip[b])) return;
+  const double* g = g_val + b * g_nnz;
+  double acc = 0.0;
+  for (int e = rowptr[r]; e < rowptr[r + 1]; ++e) acc += g[e] * x[(int64_t)b * n + col2[e]];
+  double res = alpha * acc;
+  if (z) res += beta * z[(int64_t)b * me + r];
+  y[(int64_t)b * me + r] = res;
+}
+
+// partial dot products: part[b * nb + blockIdx.x]
+__global__ void k_dot_partial(int64_t len, const double* __restrict__ a, const double* __restrict__ c,
+                              double* __restrict__ part, const int* __restrict__ skip) {
+  __shared__ double red[TPB / 32];
+  const int b = blockIdx.y;
+  double acc = 0.0;
+  if (!(skip && skip[b]))
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x)
+      acc += a[b * len + i] * c[b * len + i];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int k = 0; k < TPB / 32; ++k) t += red[k];
+    part[(int64_t)b * gridDim.x + blockIdx.x] = t;
+  }
+}
+
+constexpr int DOT_BLOCKS = 64;
+
+// CG scalar step after q = S p:  alpha = rr / (p.q)
+__global__ void k_cg_alpha(int B, const double* __restrict__ part, const double* __restrict__ rr,
+                           double* __restrict__ alpha, const int* __restrict__ done) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  if (done[b]) { alpha[b] = 0.0; return; }
+  double pq = 0.0;
+  for (int k = 0; k < DOT_BLOCKS; ++k) pq += part[(int64_t)b * DOT_BLOCKS + k];
+  alpha[b] = rr[b] / pq;
+}
+
+__global__ void k_cg_update_xr(int me, const double* __restrict__ alpha, const double* __restrict__ p,
+                               const double* __restrict__ q, double* __restrict__ x, double* __restrict__ r,
+                               const int* __restrict__ done) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (i >= me || done[b]) return;
+  const int64_t o = (int64_t)b * me + i;
+  x[o] += alpha[b] * p[o];
+  r[o] -= alpha[b] * q[o];
+}
+
+// rr_new from partials; convergence test ||r|| <= rtol ||b||; beta
+__global__ void k_cg_beta(int B, const double* __restrict__ part, double* __restrict__ rr, const double* __restrict__ bnorm2,
+                          double rtol, double* __restrict__ beta, int* __restrict__ done, int* __restrict__ iters,
+                          int* __restrict__ active) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  if (done[b]) { beta[b] = 0.0; return; }
+  double t = 0.0;
+  for (int k = 0; k < DOT_BLOCKS; ++k) t += part[(int64_t)b * DOT_BLOCKS + k];
+  iters[b] += 1;
+  beta[b] = t / rr[b];
+  rr[b] = t;
+  if (sqrt(t) <= rtol * sqrt(bnorm2[b])) done[b] = 1;
+  else atomicAdd(active, 1);
+}
+
+__global__ void k_cg_update_p(int me, const double* __restrict__ beta, const double* __restrict__ r,
+                              double* __restrict__ p, const int* __restrict__ done) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (i >= me || done[b]) return;
+  const int64_t o = (int64_t)b * me + i;
+  p[o] = r[o] + beta[b] * p[o];
+}
+
+// CG init: x = 0, r = p = bvec; rr = bnorm2 = b.b (from partials); done if b == 0
+__global__ void k_cg_init_scalars(int B, const double* __restrict__ part, double* __restrict__ rr,
+                                  double* __restrict__ bnorm2, int* __restrict__ done, int* __restrict__ iters,
+                                  const int* __restrict__ skip) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  double t = 0.0;
+  for (int k = 0; k < DOT_BLOCKS; ++k) t += part[(int64_t)b * DOT_BLOCKS + k];
+  rr[b] = t;
+  bnorm2[b] = t;
+  iters[b] = 0;
+  done[b] = (t == 0.0) || (skip && skip[b]);
+}
+
+__global__ void k_copy_neg(int64_t len, const double* __restrict__ a, double sa, double* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (i < len) out[b * len + i] = sa * a[b * len + i];
+}
+
+__global__ void k_zero(int64_t len, double* __restrict__ a) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (i < len) a[b * len + i] = 0.0;
+}
+
+// ds = -r4 - H dx ; dz = -r2 - D_s ds   (dx in internal order)
+__global__ void k_recover(int mi, int n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col2,
+                          const double* __restrict__ h_val, int64_t h_nnz, const double* __restrict__ dx,
+                          const double* __restrict__ r2, const double* __restrict__ r4, const double* __restrict__ d_s,
+                          double* __restrict__ ds, double* __restrict__ dz, const int* __restrict__ skip) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (r >= mi || (skip && skip[b])) return;
+  const double* h = h_val + b * h_nnz;
+  double acc = 0.0;
+  for (int e = rowptr[r]; e < rowptr[r + 1]; ++e) acc += h[e] * dx[(int64_t)b * n + col2[e]];
+  const int64_t o = (int64_t)b * mi + r;
+  const double s = -r4[o] - acc;
+  ds[o] = s;
+  dz[o] = -r2[o] - d_s[o] * s;
+}
+
+// ------------------------------------------------------------------------------------------
+// a8: residual of K_aug and componentwise backward error.  Row blocks x (internal), s, y, z.
+//  rho = -r - K_aug d ; ratio = |rho| / (|K_aug||d| + |r|).  Writes rho (x block internal order)
+//  and the per-row ratio / |rho| for a max reduction.
+// ------------------------------------------------------------------------------------------
+struct ResArgs {
+  int n, me, mi;
+  const int32_t* perm2;
+  const int32_t *ws_ptr, *ws_col, *ws_idx;  // symmetric W (internal), entry -> w index
+  const int32_t *gt_ptr, *gt_e, *gt_r, *ht_ptr, *ht_e, *ht_r;
+  const int32_t *g_rowptr, *g_col2, *h_rowptr, *h_col2;
+  const double *w_val, *g_val, *h_val, *sigma, *d_s, *delta;
+  int64_t w_nnz, g_nnz, h_nnz;
+  const double *r1, *r2, *r3, *r4;  // r1 original order
+  const double *dx, *ds, *dy, *dz;  // dx internal
+  double *rho1, *rho2, *rho3, *rho4;  // rho1 internal
+  double* ratio;                      // [B, rows]
+  double* absres;                     // [B, rows]
+  const int* skip;
+};
+
+__global__ void k_kaug_residual(ResArgs a) {
+  const int64_t rows = (int64_t)a.n + 2 * a.mi + a.me;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (t >= rows) return;
+  if (a.skip && a.skip[b]) { a.ratio[b * rows + t] = 0.0; a.absres[b * rows + t] = 0.0; return; }
+  const int n = a.n, me = a.me, mi = a.mi;
+  double res, den;
+  if (t < n) {
+    const int i = (int)t;
+    const int oi = a.perm2[i];
+    const double* w = a.w_val + b * a.w_nnz;
+    const double* dx = a.dx + (int64_t)b * n;
+    double acc = 0.0, aa = 0.0;
+    for (int e = a.ws_ptr[i]; e < a.ws_ptr[i + 1]; ++e) {
+      double v = w[a.ws_idx[e]] * dx[a.ws_col[e]];
+      acc += v;
+      aa += fabs(v);
+    }
+    double dg = (a.sigma[(int64_t)b * n + oi] + (a.delta ? a.delta[b] : 0.0)) * dx[i];
+    acc += dg;
+    aa += fabs(dg);
+    if (me) {
+      const double* g = a.g_val + b * a.g_nnz;
+      for (int e = a.gt_ptr[i]; e < a.gt_ptr[i + 1]; ++e) {
+        double v = g[a.gt_e[e]] * a.dy[(int64_t)b * me + a.gt_r[e]];
+        acc += v;
+        aa += fabs(v);
+      }
+    }
+    if (mi) {
+      const double* h = a.h_val + b * a.h_nnz;
+      for (int e = a.ht_ptr[i]; e < a.ht_ptr[i + 1]; ++e) {
+        double v = h[a.ht_e[e]] * a.dz[(int64_t)b * mi + a.ht_r[e]];
+        acc += v;
+        aa += fabs(v);
+      }
+    }
+    const double r = a.r1[(int64_t)b * n + oi];
+    res = -r - acc;
+    den = aa + fabs(r);
+    a.rho1[(int64_t)b * n + i] = res;
+  } else if (t < n + mi) {
+    const int r = (int)(t - n);
+    const int64_t o = (int64_t)b * mi + r;
+    const double v1 = a.d_s[o] * a.ds[o], v2 = a.dz[o];
+    res = -a.r2[o] - (v1 + v2);
+    den = fabs(v1) + fabs(v2) + fabs(a.r2[o]);
+    a.rho2[o] = res;
+  } else if (t < n + mi + me) {
+    const int r = (int)(t - n - mi);
+    const double* g = a.g_val + b * a.g_nnz;
+    const double* dx = a.dx + (int64_t)b * n;
+    double acc = 0.0, aa = 0.0;
+    for (int e = a.g_rowptr[r]; e < a.g_rowptr[r + 1]; ++e) {
+      double v = g[e] * dx[a.g_col2[e]];
+      acc += v;
+      aa += fabs(v);
+    }
+    const int64_t o = (int64_t)b * me + r;
+    res = -a.r3[o] - acc;
+    den = aa + fabs(a.r3[o]);
+    a.rho3[o] = res;
+  } else {
+    const int r = (int)(t - n - mi - me);
+    const double* h = a.h_val + b * a.h_nnz;
+    const double* dx = a.dx + (int64_t)b * n;
+    double acc = 0.0, aa = 0.0;
+    for (int e = a.h_rowptr[r]; e < a.h_rowptr[r + 1]; ++e) {
+      double v = h[e] * dx[a.h_col2[e]];
+      acc += v;
+      aa += fabs(v);
+    }
+    const int64_t o = (int64_t)b * mi + r;
+    acc += a.ds[o];
+    aa += fabs(a.ds[o]);
+    res = -a.r4[o] - acc;
+    den = aa + fabs(a.r4[o]);
+    a.rho4[o] = res;
+  }
+  double ratio = den > 0.0 ? fabs(res) / den : (res == 0.0 ? 0.0 : INFINITY);
+  if (res != res) ratio = INFINITY;
+  a.ratio[b * rows + t] = ratio;
+  a.absres[b * rows + t] = fabs(res);
+}
+
+// per-instance max over rows (two-stage; max is order independent => deterministic)
+__global__ void k_max_partial(int64_t len, const double* __restrict__ v, double* __restrict__ part) {
+  __shared__ double red[TPB / 32];
+  const int b = blockIdx.y;
+  double m = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) {
+    double x = v[b * len + i];
+    m = (x > m || x != x) ? x : m;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    double y = __shfl_down_sync(0xffffffffu, m, o);
+    m = (y > m || y != y) ? y : m;
+  }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int k = 0; k < TPB / 32; ++k) t = (red[k] > t || red[k] != red[k]) ? red[k] : t;
+    part[(int64_t)b * gridDim.x + blockIdx.x] = t;
+  }
+}
+
+__global__ void k_max_final(int B, int nb, const double* __restrict__ part, double* __restrict__ out) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  double t = 0.0;
+  for (int k = 0; k < nb; ++k) {
+    double x = part[(int64_t)b * nb + k];
+    t = (x > t || x != x) ? x : t;
+  }
+  out[b] = t;
+}
+
+// d_new = d + c for accepted instances; dest <- src where acc[b]
+__global__ void k_axpy_sel(int64_t len, const double* __restrict__ d, const double* __restrict__ c,
+                           double* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (i < len) out[b * len + i] = d[b * len + i] + c[b * len + i];
+}
+
+__global__ void k_copy_sel(int64_t len, const double* __restrict__ src, double* __restrict__ dst,
+                           const int* __restrict__ acc) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (i < len && acc[b]) dst[b * len + i] = src[b * len + i];
+}
+
+// dx (original order) = dx_int[iperm]; NaN for NOT_PD instances
+__global__ void k_unpermute(int n, const int32_t* __restrict__ perm2, const double* __restrict__ xi,
+                            double* __restrict__ xo, const int* __restrict__ notpd) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (j >= n) return;
+  xo[(int64_t)b * n + perm2[j]] = notpd[b] ? nan("") : xi[(int64_t)b * n + j];
+}
+
+__global__ void k_nan_fill(int64_t len, double* __restrict__ a, const int* __restrict__ notpd) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (i < len && notpd[b]) a[b * len + i] = nan("");
+}
+
+template <class T>
+T* upload(const std::vector<T>& v, std::vector<void*>& owned, int64_t& bytes) {
+  size_t sz = std::max<size_t>(1, v.size()) * sizeof(T);
+  void* p = nullptr;
+  if (cudaMalloc(&p, sz) != cudaSuccess) return nullptr;
+  owned.push_back(p);
+  bytes += sz;
+  if (!v.empty()) cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+  return (T*)p;
+}
+
+}  // namespace
+
+// ============================================================================================
+// context
+// ============================================================================================
+struct ckkt_ctx {
+  ckkt::Analysis A;
+  ckkt_options opt{};
+  int B = 1;
+  bool has_device = false;
+  cudaStream_t stream = nullptr;
+  int64_t nnzk = 0, Lsize = 0, w_nnz = 0, g_nnz = 0, h_nnz = 0;
+  int n = 0, me = 0, mi = 0;
+  int max_w = 1;
+  std::vector<void*> owned;
+  int64_t device_bytes = 0;
+  int64_t launches = 0;
+  // pattern arrays on device
+  SymDev S{};
+  int64_t *wt_ptr = nullptr, *jt_ptr = nullptr;
+  int32_t *wt_idx = nullptr, *jt_a = nullptr, *jt_b = nullptr, *jt_r = nullptr, *kdiag = nullptr;
+  int32_t *gt_ptr = nullptr, *gt_e = nullptr, *gt_r = nullptr, *ht_ptr = nullptr, *ht_e = nullptr, *ht_r = nullptr;
+  int32_t *g_rowptr = nullptr, *g_col2 = nullptr, *h_rowptr = nullptr, *h_col2 = nullptr;
+  int32_t *ws_ptr = nullptr, *ws_col = nullptr, *ws_idx = nullptr;
+  // numeric
+  double *Kval = nullptr, *L = nullptr;
+  int *notpd = nullptr, *minpiv = nullptr;
+  // last refactor values (caller-owned, must stay valid until the next refactor)
+  const double *w_val = nullptr, *g_val = nullptr, *h_val = nullptr, *sigma = nullptr, *d_s = nullptr,
+               *delta = nullptr;
+  bool factored = false;
+  // work vectors
+  double *rg = nullptr, *tn = nullptr, *vn = nullptr;             // [B,n]
+  double *cg_x = nullptr, *cg_r = nullptr, *cg_p = nullptr, *cg_q = nullptr, *bvec = nullptr;  // [B,me]
+  double *dxi = nullptr, *dxi2 = nullptr, *cdx = nullptr;         // [B,n] step, trial, correction (internal)
+  double *ds2 = nullptr, *dy2 = nullptr, *dz2 = nullptr;          // trial blocks
+  double *cds = nullptr, *cdy = nullptr, *cdz = nullptr;          // correction blocks
+  double *rho1 = nullptr, *rho2 = nullptr, *rho3 = nullptr, *rho4 = nullptr;
+  double *rho1b = nullptr, *rho2b = nullptr, *rho3b = nullptr, *rho4b = nullptr;
+  double *ratio = nullptr, *absres = nullptr, *part = nullptr, *omega = nullptr, *resinf = nullptr;
+  double *cg_rr = nullptr, *cg_bn = nullptr, *cg_alpha = nullptr, *cg_beta = nullptr;
+  int *cg_done = nullptr, *cg_iters = nullptr, *active = nullptr, *accflag = nullptr, *skipflag = nullptr;
+  int* h_pinned_int = nullptr;
+  double* h_pinned_dbl = nullptr;
+  // host-staging buffers for ckkt_iterate_host
+  double *st_w = nullptr, *st_g = nullptr, *st_h = nullptr, *st_sig = nullptr, *st_ds = nullptr, *st_del = nullptr;
+  double *st_r1 = nullptr, *st_r2 = nullptr, *st_r3 = nullptr, *st_r4 = nullptr;
+  double *st_dx = nullptr, *st_ds_o = nullptr, *st_dy = nullptr, *st_dz = nullptr;
+  int* st_notpd = nullptr;
+};
+
+namespace {
+
+ckkt_status dalloc(ckkt_ctx* c, void** p, size_t bytes) {
+  if (bytes == 0) bytes = 8;
+  if (cudaMalloc(p, bytes) != cudaSuccess) return CKKT_OUT_OF_MEMORY;
+  c->owned.push_back(*p);
+  c->device_bytes += bytes;
+  return CKKT_OK;
+}
+
+#define DALLOC(ptr, count)                                                        \
+  do {                                                                            \
+    ckkt_status st_ = dalloc(c, (void**)&(ptr), (size_t)(count) * sizeof(*(ptr))); \
+    if (st_ != CKKT_OK) return st_;                                               \
+  } while (0)
+
+ckkt_status setup_device(ckkt_ctx* c) {
+  ckkt::Analysis& A = c->A;
+  const int B = c->B;
+  const int n = c->n, me = c->me, mi = c->mi;
+  CK(cudaSetDevice(c->opt.device));
+  c->stream = (cudaStream_t)c->opt.stream;
+  std::vector<void*>& o = c->owned;
+  int64_t& by = c->device_bytes;
+#define UP(dst, vec)                          \
+  do {                                        \
+    dst = upload(vec, o, by);                 \
+    if (!dst) return CKKT_OUT_OF_MEMORY;      \
+  } while (0)
+  int32_t *sfirst, *srows, *level_list, *upd_ptr, *upd_d, *upd_p, *upd_q, *relmap, *kmap, *perm2;
+  int64_t *srowptr, *pofs, *upd_rel, *kp;
+  UP(sfirst, A.sfirst);
+  UP(srowptr, A.srowptr);
+  UP(srows, A.srows);
+  UP(pofs, A.pofs);
+  UP(level_list, A.level_list);
+  UP(upd_ptr, A.upd_ptr);
+  UP(upd_d, A.upd_d);
+  UP(upd_p, A.upd_p);
+  UP(upd_q, A.upd_q);
+  UP(upd_rel, A.upd_rel);
+  UP(relmap, A.relmap);
+  UP(kp, A.kp);
+  UP(kmap, A.kmap);
+  UP(perm2, A.perm2);
+  c->S = SymDev{sfirst, srowptr, srows, pofs, level_list, upd_ptr, upd_d, upd_p, upd_q, upd_rel, relmap, kp, kmap, perm2};
+  UP(c->wt_ptr, A.wt_ptr);
+  UP(c->wt_idx, A.wt_idx);
+  UP(c->jt_ptr, A.jt_ptr);
+  UP(c->jt_a, A.jt_a);
+  UP(c->jt_b, A.jt_b);
+  UP(c->jt_r, A.jt_r);
+  std::vector<int32_t> kdiag(c->nnzk, -1);
+  for (int j = 0; j < n; ++j) kdiag[A.dslot[j]] = A.perm2[j];
+  UP(c->kdiag, kdiag);
+  UP(c->gt_ptr, A.gt_ptr);
+  UP(c->gt_e, A.gt_e);
+  UP(c->gt_r, A.gt_r);
+  UP(c->ht_ptr, A.ht_ptr);
+  UP(c->ht_e, A.ht_e);
+  UP(c->ht_r, A.ht_r);
+  UP(c->g_rowptr, A.pat.g_rowptr);
+  UP(c->g_col2, A.g_col2);
+  UP(c->h_rowptr, A.pat.h_rowptr);
+  UP(c->h_col2, A.h_col2);
+  // symmetric W rows (internal order), entries sorted by (row, col, w index)
+  {
+    std::vector<std::array<int32_t, 3>> ent;
+    ent.reserve(2 * A.w_row2.size());
+    for (size_t e = 0; e < A.w_row2.size(); ++e) {
+      ent.push_back({A.w_row2[e], A.w_col2[e], (int32_t)e});
+      if (A.w_row2[e] != A.w_col2[e]) ent.push_back({A.w_col2[e], A.w_row2[e], (int32_t)e});
+    }
+    std::sort(ent.begin(), ent.end());
+    std::vector<int32_t> ptr(n + 1, 0), col(ent.size()), idx(ent.size());
+    for (size_t k = 0; k < ent.size(); ++k) {
+      ptr[ent[k][0] + 1]++;
+      col[k] = ent[k][1];
+      idx[k] = ent[k][2];
+    }
+    for (int i = 0; i < n; ++i) ptr[i + 1] += ptr[i];
+    UP(c->ws_ptr, ptr);
+    UP(c->ws_col, col);
+    UP(c->ws_idx, idx);
+  }
+#undef UP
+  DALLOC(c->Kval, (size_t)B * c->nnzk);
+  DALLOC(c->L, (size_t)B * c->Lsize);
+  DALLOC(c->notpd, B);
+  DALLOC(c->minpiv, B);
+  const size_t Bn = (size_t)B * n, Bme = (size_t)B * std::max(me, 1), Bmi = (size_t)B * std::max(mi, 1);
+  DALLOC(c->rg, Bn);
+  DALLOC(c->tn, Bn);
+  DALLOC(c->vn, Bn);
+  DALLOC(c->cg_x, Bme);
+  DALLOC(c->cg_r, Bme);
+  DALLOC(c->cg_p, Bme);
+  DALLOC(c->cg_q, Bme);
+  DALLOC(c->bvec, Bme);
+  DALLOC(c->dxi, Bn);
+  DALLOC(c->dxi2, Bn);
+  DALLOC(c->cdx, Bn);
+  DALLOC(c->ds2, Bmi);
+  DALLOC(c->dy2, Bme);
+  DALLOC(c->dz2, Bmi);
+  DALLOC(c->cds, Bmi);
+  DALLOC(c->cdy, Bme);
+  DALLOC(c->cdz, Bmi);
+  DALLOC(c->rho1, Bn);
+  DALLOC(c->rho2, Bmi);
+  DALLOC(c->rho3, Bme);
+  DALLOC(c->rho4, Bmi);
+  DALLOC(c->rho1b, Bn);
+  DALLOC(c->rho2b, Bmi);
+  DALLOC(c->rho3b, Bme);
+  DALLOC(c->rho4b, Bmi);
+  const size_t rows = (size_t)n + 2 * (size_t)mi + me;
+  DALLOC(c->ratio, (size_t)B * rows);
+  DALLOC(c->absres, (size_t)B * rows);
+  DALLOC(c->part, (size_t)B * 1024);
+  DALLOC(c->omega, 2 * B);
+  DALLOC(c->resinf, 2 * B);
+  DALLOC(c->cg_rr, B);
+  DALLOC(c->cg_bn, B);
+  DALLOC(c->cg_alpha, B);
+  DALLOC(c->cg_beta, B);
+  DALLOC(c->cg_done, B);
+  DALLOC(c->cg_iters, B);
+  DALLOC(c->active, 1);
+  DALLOC(c->accflag, B);
+  DALLOC(c->skipflag, B);
+  CK(cudaMallocHost(&c->h_pinned_int, sizeof(int) * (5 * B + 16)));
+  CK(cudaMallocHost(&c->h_pinned_dbl, sizeof(double) * (8 * B + 16)));
+  return CKKT_OK;
+}
+
+}  // namespace
+
+// ============================================================================================
+// C ABI
+// ============================================================================================
+extern "C" {
+
+void ckkt_default_options(ckkt_options* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->strategy = CKKT_HYKKT;
+  o->gamma = 1e7;
+  o->cg_rtol = 1e-10;
+  o->cg_maxit = 200;
+  o->ref_tol = 1e-14;
+  o->ref_maxit = 10;
+  o->batch = 1;
+  o->leaf = 64;
+  o->perm = nullptr;
+  o->device = 0;
+  o->stream = nullptr;
+}
+
+const char* ckkt_status_str(ckkt_status s) {
+  switch (s) {
+    case CKKT_OK: return "ok";
+    case CKKT_NOT_PD: return "not positive definite (wrong inertia)";
+    case CKKT_CG_NO_CONVERGENCE: return "CG did not converge";
+    case CKKT_REFINE_NOT_CONVERGED: return "refinement did not reach ref_tol";
+    case CKKT_PATTERN_ERROR: return "pattern error";
+    case CKKT_INVALID_ARG: return "invalid argument";
+    case CKKT_CUDA_ERROR: return "CUDA error";
+    case CKKT_OUT_OF_MEMORY: return "out of memory";
+  }
+  return "unknown";
+}
+
+void ckkt_destroy(ckkt_ctx* c) {
+  if (!c) return;
+  if (c->has_device) {
+    cudaSetDevice(c->opt.device);
+    for (void* p : c->owned) cudaFree(p);
+    if (c->h_pinned_int) cudaFreeHost(c->h_pinned_int);
+    if (c->h_pinned_dbl) cudaFreeHost(c->h_pinned_dbl);
+  }
+  delete c;
+}
+
+ckkt_status ckkt_setup(const ckkt_pattern* p, const ckkt_options* opt, ckkt_ctx** out) {
+  if (!p || !out) return CKKT_INVALID_ARG;
+  *out = nullptr;
+  ckkt_options o;
+  if (opt) o = *opt;
+  else ckkt_default_options(&o);
+  if (o.batch < 1 || (o.strategy != CKKT_LIFTED && o.strategy != CKKT_HYKKT)) return CKKT_INVALID_ARG;
+  if (o.strategy == CKKT_LIFTED && p->m_e != 0) return CKKT_INVALID_ARG;
+  if (p->n <= 0 || p->m_e < 0 || p->m_i < 0 || p->w_nnz < 0) return CKKT_INVALID_ARG;
+  if ((p->w_nnz > 0 && (!p->w_row || !p->w_col)) || (p->m_e > 0 && (!p->g_rowptr || !p->g_col)) ||
+      (p->m_i > 0 && (!p->h_rowptr || !p->h_col)))
+    return CKKT_INVALID_ARG;
+  std::unique_ptr<ckkt_ctx> c(new ckkt_ctx());
+  c->opt = o;
+  c->B = o.batch;
+  ckkt::Pattern pat;
+  pat.n = p->n;
+  pat.me = p->m_e;
+  pat.mi = p->m_i;
+  pat.w_row.assign(p->w_row, p->w_row + p->w_nnz);
+  pat.w_col.assign(p->w_col, p->w_col + p->w_nnz);
+  if (p->m_e > 0) {
+    pat.g_rowptr.assign(p->g_rowptr, p->g_rowptr + p->m_e + 1);
+    pat.g_col.assign(p->g_col, p->g_col + pat.g_rowptr.back());
+  } else {
+    pat.g_rowptr.assign(1, 0);
+  }
+  if (p->m_i > 0) {
+    pat.h_rowptr.assign(p->h_rowptr, p->h_rowptr + p->m_i + 1);
+    pat.h_col.assign(p->h_col, p->h_col + pat.h_rowptr.back());
+  } else {
+    pat.h_rowptr.assign(1, 0);
+  }
+  int code = 0;
+  std::string err = ckkt::analyze(pat, o.leaf > 0 ? o.leaf : 64, o.perm, c->A, code);
+  if (!err.empty()) return (ckkt_status)code;
+  c->n = p->n;
+  c->me = p->m_e;
+  c->mi = p->m_i;
+  c->nnzk = c->A.kp[c->n];
+  c->Lsize = c->A.pofs[c->A.ns];
+  if (c->Lsize >= ((int64_t)1 << 31)) return CKKT_OUT_OF_MEMORY;
+  c->w_nnz = p->w_nnz;
+  c->g_nnz = c->A.pat.g_rowptr.back();
+  c->h_nnz = c->A.pat.h_rowptr.back();
+  for (int s = 0; s < c->A.ns; ++s) c->max_w = std::max(c->max_w, c->A.sfirst[s + 1] - c->A.sfirst[s]);
+  if (c->max_w * 8 > 48 * 1024) return CKKT_INVALID_ARG;
+  if (o.device >= 0) {
+    c->has_device = true;
+    ckkt_status st = setup_device(c.get());
+    if (st != CKKT_OK) {
+      ckkt_destroy(c.release());
+      return st;
+    }
+  }
+  *out = c.release();
+  return CKKT_OK;
+}
+
+ckkt_status ckkt_get_sizes(const ckkt_ctx* c, ckkt_sizes* s) {
+  if (!c || !s) return CKKT_INVALID_ARG;
+  s->n = c->n;
+  s->m_e = c->me;
+  s->m_i = c->mi;
+  s->batch = c->B;
+  s->nnz_k = c->nnzk;
+  s->nnz_l = c->A.nnz_l;
+  s->l_storage = c->Lsize;
+  s->n_supernodes = c->A.ns;
+  s->n_levels = c->A.nlevels;
+  s->flops_factor = c->A.flops;
+  s->device_bytes = c->device_bytes;
+  return CKKT_OK;
+}
+
+ckkt_status ckkt_export_symbolic(const ckkt_ctx* c, int32_t* perm, int32_t* parent, int32_t* colcount,
+                                 int64_t* l_colptr, int32_t* l_rowind) {
+  if (!c) return CKKT_INVALID_ARG;
+  const int n = c->n;
+  if (perm) std::copy(c->A.perm.begin(), c->A.perm.end(), perm);
+  if (parent) std::copy(c->A.parent.begin(), c->A.parent.end(), parent);
+  if (colcount) std::copy(c->A.colcount.begin(), c->A.colcount.end(), colcount);
+  if (l_colptr || l_rowind) {
+    std::vector<int64_t> Lp;
+    std::vector<int32_t> Li;
+    ckkt::export_l_pattern(c->A, Lp, Li);
+    if (l_colptr) std::copy(Lp.begin(), Lp.end(), l_colptr);
+    if (l_rowind) std::copy(Li.begin(), Li.end(), l_rowind);
+  }
+  (void)n;
+  return CKKT_OK;
+}
+
+int64_t ckkt_launch_count(const ckkt_ctx* c) { return c ? c->launches : 0; }
+
+ckkt_status ckkt_refactor(ckkt_ctx* c, const double* w_val, const double* g_val, const double* h_val,
+                          const double* sigma_x, const double* d_s, const double* delta_x, int32_t* not_pd,
+                          int32_t* min_bad_pivot) {
+  if (!c || !c->has_device) return CKKT_INVALID_ARG;
+  if ((c->w_nnz && !w_val) || !sigma_x || (c->g_nnz && !g_val) || (c->h_nnz && !h_val) || (c->mi && !d_s))
+    return CKKT_INVALID_ARG;
+  CK(cudaSetDevice(c->opt.device));
+  cudaStream_t st = c->stream;
+  const int B = c->B;
+  c->w_val = w_val;
+  c->g_val = g_val;
+  c->h_val = h_val;
+  c->sigma = sigma_x;
+  c->d_s = d_s;
+  c->delta = delta_x;
+  const double gamma = (c->opt.strategy == CKKT_HYKKT) ? c->opt.gamma : 0.0;
+  k_init_flags<<<nblk(B), TPB, 0, st>>>(B, c->notpd, c->minpiv);
+  k_condense<<<dim3(nblk(c->nnzk), B), TPB, 0, st>>>(c->nnzk, c->wt_ptr, c->wt_idx, c->jt_ptr, c->jt_a, c->jt_b,
+                                                     c->jt_r, c->kdiag, w_val, c->w_nnz, g_val, c->g_nnz, h_val,
+                                                     c->h_nnz, sigma_x, d_s, delta_x, gamma, c->n, c->me, c->mi,
+                                                     c->Kval);
+  c->launches += 2;
+  const auto& A = c->A;
+  for (int l = 0; l < A.nlevels; ++l) {
+    int cnt = A.level_ptr[l + 1] - A.level_ptr[l];
+    k_factor<<<dim3(cnt, B), 128, 0, st>>>(c->S, A.level_ptr[l], c->L, c->Lsize, c->Kval, c->nnzk, c->notpd,
+                                           c->minpiv);
+    c->launches++;
+  }
+  k_final_flags<<<nblk(B), TPB, 0, st>>>(B, c->notpd, c->minpiv, c->S.perm2, not_pd, min_bad_pivot);
+  c->launches++;
+  CK(cudaGetLastError());
+  c->factored = true;
+  return CKKT_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// x <- K^{-1} x  (internal order, in place), skipping instances with skip[b]
+void ksolve(ckkt_ctx* c, double* x, const int* skip) {
+  const auto& A = c->A;
+  cudaStream_t st = c->stream;
+  const size_t sm = sizeof(double) * c->max_w;
+  for (int l = 0; l < A.nlevels; ++l) {
+    int cnt = A.level_ptr[l + 1] - A.level_ptr[l];
+    k_fwd<<<dim3(cnt, c->B), 128, sm, st>>>(c->S, A.level_ptr[l], c->L, c->Lsize, x, c->n, skip);
+  }
+  for (int l = A.nlevels - 1; l >= 0; --l) {
+    int cnt = A.level_ptr[l + 1] - A.level_ptr[l];
+    k_bwd<<<dim3(cnt, c->B), TPB, sm, st>>>(c->S, A.level_ptr[l], c->L, c->Lsize, x, c->n, skip);
+  }
+  c->launches += 2 * A.nlevels;
+}
+
+void dot(ckkt_ctx* c, int64_t len, const double* a, const double* b, const int* skip) {
+  k_dot_partial<<<dim3(DOT_BLOCKS, c->B), TPB, 0, c->stream>>>(len, a, b, c->part, skip);
+  c->launches++;
+}
+
+// One unrefined pass of the strategy for right-hand side (r1 [internal if r1_internal], r2, r3, r4):
+// writes dx (internal), ds, dy, dz.  Returns the total CG iterations (host copy, per instance) via c->cg_iters.
+ckkt_status solve_pass(ckkt_ctx* c, const double* r1, int r1_internal, const double* r2, const double* r3,
+                       const double* r4, double* dx, double* ds, double* dy, double* dz, const int* skip,
+                       std::vector<int>& kcg) {
+  const int n = c->n, me = c->me, mi = c->mi, B = c->B;
+  cudaStream_t st = c->stream;
+  const double gamma = (c->opt.strategy == CKKT_HYKKT) ? c->opt.gamma : 0.0;
+  const dim3 gn(nblk(n), B), gme(nblk(std::max(me, 1)), B), gmi(nblk(std::max(mi, 1)), B);
+  // r_gamma (or r~) in internal order, into dx (it becomes -K^{-1}(...) after the solves)
+  k_rhs<<<gn, TPB, 0, st>>>(n, me, mi, c->S.perm2, r1, r1_internal, r2, r3, r4, c->gt_ptr, c->gt_e, c->gt_r,
+                            c->ht_ptr, c->ht_e, c->ht_r, c->g_val, c->g_nnz, c->h_val, c->h_nnz, c->d_s, gamma, c->rg,
+                            skip);
+  c->launches++;
+  kcg.assign(B, 0);
+  if (me > 0) {
+    // t = K^{-1} r_gamma ; b = r3 - G t
+    cudaMemcpyAsync(c->tn, c->rg, sizeof(double) * (size_t)B * n, cudaMemcpyDeviceToDevice, st);
+    ksolve(c, c->tn, skip);
+    k_g_spmv<<<gme, TPB, 0, st>>>(me, n, c->g_rowptr, c->g_col2, c->g_val, c->g_nnz, c->tn, -1.0, r3, 1.0, c->bvec,
+                                  skip);
+    // CG: x = 0, r = p = b
+    k_zero<<<gme, TPB, 0, st>>>(me, c->cg_x);
+    cudaMemcpyAsync(c->cg_r, c->bvec, sizeof(double) * (size_t)B * me, cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(c->cg_p, c->bvec, sizeof(double) * (size_t)B * me, cudaMemcpyDeviceToDevice, st);
+    dot(c, me, c->bvec, c->bvec, skip);
+    k_cg_init_scalars<<<nblk(B), TPB, 0, st>>>(B, c->part, c->cg_rr, c->cg_bn, c->cg_done, c->cg_iters, skip);
+    c->launches += 4;
+    for (int it = 0; it < c->opt.cg_maxit; ++it) {
+      // q = G K^{-1} G^T p
+      k_gt_spmv<<<gn, TPB, 0, st>>>(n, me, c->gt_ptr, c->gt_e, c->gt_r, c->g_val, c->g_nnz, c->cg_p, 1.0, nullptr,
+                                    0.0, c->vn, c->cg_done);
+      ksolve(c, c->vn, c->cg_done);
+      k_g_spmv<<<gme, TPB, 0, st>>>(me, n, c->g_rowptr, c->g_col2, c->g_val, c->g_nnz, c->vn, 1.0, nullptr, 0.0,
+                                    c->cg_q, c->cg_done);
+      dot(c, me, c->cg_p, c->cg_q, c->cg_done);
+      k_cg_alpha<<<nblk(B), TPB, 0, st>>>(B, c->part, c->cg_rr, c->cg_alpha, c->cg_done);
+      k_cg_update_xr<<<gme, TPB, 0, st>>>(me, c->cg_alpha, c->cg_p, c->cg_q, c->cg_x, c->cg_r, c->cg_done);
+      dot(c, me, c->cg_r, c->cg_r, c->cg_done);
+      cudaMemsetAsync(c->active, 0, sizeof(int), st);
+      k_cg_beta<<<nblk(B), TPB, 0, st>>>(B, c->part, c->cg_rr, c->cg_bn, c->opt.cg_rtol, c->cg_beta, c->cg_done,
+                                         c->cg_iters, c->active);
+      k_cg_update_p<<<gme, TPB, 0, st>>>(me, c->cg_beta, c->cg_r, c->cg_p, c->cg_done);
+      c->launches += 7;
+      int* h_active = c->h_pinned_int + 4 * B;
+      CK(cudaMemcpyAsync(h_active, c->active, sizeof(int), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      if (*h_active == 0) break;
+    }
+    // dy = x ; dx = K^{-1}(-r_gamma - G^T dy)
+    cudaMemcpyAsync(dy, c->cg_x, sizeof(double) * (size_t)B * me, cudaMemcpyDeviceToDevice, st);
+    k_gt_spmv<<<gn, TPB, 0, st>>>(n, me, c->gt_ptr, c->gt_e, c->gt_r, c->g_val, c->g_nnz, dy, -1.0, c->rg, -1.0, dx,
+                                  skip);
+    c->launches++;
+    ksolve(c, dx, skip);
+    int* h_iters = c->h_pinned_int + 3 * B;
+    CK(cudaMemcpyAsync(h_iters, c->cg_iters, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int b = 0; b < B; ++b) kcg[b] = h_iters[b];
+  } else {
+    k_copy_neg<<<gn, TPB, 0, st>>>(n, c->rg, -1.0, dx);
+    c->launches++;
+    ksolve(c, dx, skip);
+  }
+  if (mi > 0) {
+    k_recover<<<gmi, TPB, 0, st>>>(mi, n, c->h_rowptr, c->h_col2, c->h_val, c->h_nnz, dx, r2, r4, c->d_s, ds, dz,
+                                   skip);
+    c->launches++;
+  }
+  CK(cudaGetLastError());
+  return CKKT_OK;
+}
+
+// residual of (dx internal, ds, dy, dz) against r (r1 original order); omega/resinf [B] device at offset
+void residual(ckkt_ctx* c, const double* r1, const double* r2, const double* r3, const double* r4, const double* dx,
+              const double* ds, const double* dy, const double* dz, double* rho1, double* rho2, double* rho3,
+              double* rho4, double* omega, double* resinf) {
+  const int n = c->n, me = c->me, mi = c->mi, B = c->B;
+  const int64_t rows = (int64_t)n + 2 * mi + me;
+  ResArgs a;
+  a.n = n; a.me = me; a.mi = mi;
+  a.perm2 = c->S.perm2;
+  a.ws_ptr = c->ws_ptr; a.ws_col = c->ws_col; a.ws_idx = c->ws_idx;
+  a.gt_ptr = c->gt_ptr; a.gt_e = c->gt_e; a.gt_r = c->gt_r;
+  a.ht_ptr = c->ht_ptr; a.ht_e = c->ht_e; a.ht_r = c->ht_r;
+  a.g_rowptr = c->g_rowptr; a.g_col2 = c->g_col2; a.h_rowptr = c->h_rowptr; a.h_col2 = c->h_col2;
+  a.w_val = c->w_val; a.g_val = c->g_val; a.h_val = c->h_val; a.sigma = c->sigma; a.d_s = c->d_s; a.delta = c->delta;
+  a.w_nnz = c->w_nnz; a.g_nnz = c->g_nnz; a.h_nnz = c->h_nnz;
+  a.r1 = r1; a.r2 = r2; a.r3 = r3; a.r4 = r4;
+  a.dx = dx; a.ds = ds; a.dy = dy; a.dz = dz;
+  a.rho1 = rho1; a.rho2 = rho2; a.rho3 = rho3; a.rho4 = rho4;
+  a.ratio = c->ratio; a.absres = c->absres;
+  a.skip = c->notpd;
+  cudaStream_t st = c->stream;
+  k_kaug_residual<<<dim3(nblk(rows), B), TPB, 0, st>>>(a);
+  k_max_partial<<<dim3(DOT_BLOCKS, B), TPB, 0, st>>>(rows, c->ratio, c->part);
+  k_max_final<<<nblk(B), TPB, 0, st>>>(B, DOT_BLOCKS, c->part, omega);
+  k_max_partial<<<dim3(DOT_BLOCKS, B), TPB, 0, st>>>(rows, c->absres, c->part);
+  k_max_final<<<nblk(B), TPB, 0, st>>>(B, DOT_BLOCKS, c->part, resinf);
+  c->launches += 5;
+}
+
+}  // namespace
+
+extern "C" ckkt_status ckkt_solve(ckkt_ctx* c, const double* r1, const double* r2, const double* r3, const double* r4,
+                                  double* dx, double* ds, double* dy, double* dz, ckkt_info* info) {
+  if (!c || !c->has_device || !c->factored) return CKKT_INVALID_ARG;
+  const int n = c->n, me = c->me, mi = c->mi, B = c->B;
+  if (!r1 || !dx || (me && (!r3 || !dy)) || (mi && (!r2 || !r4 || !ds || !dz))) return CKKT_INVALID_ARG;
+  CK(cudaSetDevice(c->opt.device));
+  cudaStream_t st = c->stream;
+  const dim3 gn(nblk(n), B), gme(nblk(std::max(me, 1)), B), gmi(nblk(std::max(mi, 1)), B);
+  std::vector<int> kcg, kcg_total(B, 0), nref(B, 0);
+  // unrefined pass: step in (dxi, ds, dy, dz)
+  ckkt_status s = solve_pass(c, r1, 0, r2, r3, r4, c->dxi, ds, dy, dz, c->notpd, kcg);
+  if (s != CKKT_OK) return s;
+  for (int b = 0; b < B; ++b) kcg_total[b] = kcg[b];
+  std::vector<int> kcg0 = kcg;
+  residual(c, r1, r2, r3, r4, c->dxi, ds, dy, dz, c->rho1, c->rho2, c->rho3, c->rho4, c->omega, c->resinf);
+  CK(cudaMemcpyAsync(c->h_pinned_dbl, c->omega, sizeof(double) * B, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(c->h_pinned_dbl + B, c->resinf, sizeof(double) * B, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(c->h_pinned_int, c->notpd, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  std::vector<double> omega(B), omega0(B), prev(B), rinf(B);
+  std::vector<int> notpd(B), done(B, 0);
+  for (int b = 0; b < B; ++b) {
+    omega[b] = omega0[b] = prev[b] = c->h_pinned_dbl[b];
+    rinf[b] = c->h_pinned_dbl[B + b];
+    notpd[b] = c->h_pinned_int[b];
+    done[b] = notpd[b] || !(omega[b] > c->opt.ref_tol);
+  }
+  for (int it = 0; it < c->opt.ref_maxit; ++it) {
+    bool any = false;
+    for (int b = 0; b < B; ++b) any |= !done[b];
+    if (!any) break;
+    int* h_skip = c->h_pinned_int + B;  // previous H2D copies from this region completed at the last sync
+    for (int b = 0; b < B; ++b) h_skip[b] = done[b];
+    CK(cudaMemcpyAsync(c->skipflag, h_skip, sizeof(int) * B, cudaMemcpyHostToDevice, st));
+    // correction: solve K_aug delta = rho  (i.e. right-hand side "r" = -rho)
+    k_copy_neg<<<gn, TPB, 0, st>>>(n, c->rho1, -1.0, c->rho1b);
+    if (mi) {
+      k_copy_neg<<<gmi, TPB, 0, st>>>(mi, c->rho2, -1.0, c->rho2b);
+      k_copy_neg<<<gmi, TPB, 0, st>>>(mi, c->rho4, -1.0, c->rho4b);
+    }
+    if (me) k_copy_neg<<<gme, TPB, 0, st>>>(me, c->rho3, -1.0, c->rho3b);
+    c->launches += 4;
+    s = solve_pass(c, c->rho1b, 1, c->rho2b, c->rho3b, c->rho4b, c->cdx, c->cds, c->cdy, c->cdz, c->skipflag, kcg);
+    if (s != CKKT_OK) return s;
+    // trial = d + correction
+    k_axpy_sel<<<gn, TPB, 0, st>>>(n, c->dxi, c->cdx, c->dxi2);
+    if (mi) {
+      k_axpy_sel<<<gmi, TPB, 0, st>>>(mi, ds, c->cds, c->ds2);
+      k_axpy_sel<<<gmi, TPB, 0, st>>>(mi, dz, c->cdz, c->dz2);
+    }
+    if (me) k_axpy_sel<<<gme, TPB, 0, st>>>(me, dy, c->cdy, c->dy2);
+    c->launches += 4;
+    residual(c, r1, r2, r3, r4, c->dxi2, c->ds2, c->dy2, c->dz2, c->rho1b, c->rho2b, c->rho3b, c->rho4b,
+             c->omega + B, c->resinf + B);
+    CK(cudaMemcpyAsync(c->h_pinned_dbl + 2 * B, c->omega + B, sizeof(double) * B, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(c->h_pinned_dbl + 3 * B, c->resinf + B, sizeof(double) * B, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int b = 0; b < B; ++b) {
+      int acc = 0;
+      if (!done[b]) {
+        double om = c->h_pinned_dbl[2 * B + b];
+        nref[b]++;
+        kcg_total[b] += kcg[b];
+        if (om < omega[b]) {
+          acc = 1;
+          omega[b] = om;
+          rinf[b] = c->h_pinned_dbl[3 * B + b];
+        }
+        if (!(om > c->opt.ref_tol) || om > 0.5 * prev[b]) done[b] = 1;
+        prev[b] = om;
+      }
+      c->h_pinned_int[2 * B + b] = acc;
+    }
+    CK(cudaMemcpyAsync(c->accflag, c->h_pinned_int + 2 * B, sizeof(int) * B, cudaMemcpyHostToDevice, st));
+    k_copy_sel<<<gn, TPB, 0, st>>>(n, c->dxi2, c->dxi, c->accflag);
+    k_copy_sel<<<gn, TPB, 0, st>>>(n, c->rho1b, c->rho1, c->accflag);
+    if (mi) {
+      k_copy_sel<<<gmi, TPB, 0, st>>>(mi, c->ds2, ds, c->accflag);
+      k_copy_sel<<<gmi, TPB, 0, st>>>(mi, c->dz2, dz, c->accflag);
+      k_copy_sel<<<gmi, TPB, 0, st>>>(mi, c->rho2b, c->rho2, c->accflag);
+      k_copy_sel<<<gmi, TPB, 0, st>>>(mi, c->rho4b, c->rho4, c->accflag);
+    }
+    if (me) {
+      k_copy_sel<<<gme, TPB, 0, st>>>(me, c->dy2, dy, c->accflag);
+      k_copy_sel<<<gme, TPB, 0, st>>>(me, c->rho3b, c->rho3, c->accflag);
+    }
+    c->launches += 8;
+  }
+  k_unpermute<<<gn, TPB, 0, st>>>(n, c->S.perm2, c->dxi, dx, c->notpd);
+  if (mi) {
+    k_nan_fill<<<gmi, TPB, 0, st>>>(mi, ds, c->notpd);
+    k_nan_fill<<<gmi, TPB, 0, st>>>(mi, dz, c->notpd);
+  }
+  if (me) k_nan_fill<<<gme, TPB, 0, st>>>(me, dy, c->notpd);
+  c->launches += 4;
+  CK(cudaGetLastError());
+  ckkt_status worst = CKKT_OK;
+  if (info) {
+    CK(cudaStreamSynchronize(st));
+    for (int b = 0; b < B; ++b) {
+      ckkt_info& I = info[b];
+      I.k_cg = kcg0[b];
+      I.k_cg_total = kcg_total[b];
+      I.n_ref = nref[b];
+      I.rel_res = omega[b];
+      I.rel_res_unrefined = omega0[b];
+      I.res_inf = rinf[b];
+      ckkt_status sb = CKKT_OK;
+      if (notpd[b]) sb = CKKT_NOT_PD;
+      else if (me && kcg0[b] >= c->opt.cg_maxit) sb = CKKT_CG_NO_CONVERGENCE;
+      else if (c->opt.ref_maxit > 0 && omega[b] > c->opt.ref_tol && omega[b] > 1e-10) sb = CKKT_REFINE_NOT_CONVERGED;
+      I.status = sb;
+      if (sb != CKKT_OK && (worst == CKKT_OK || sb == CKKT_NOT_PD)) worst = sb;
+    }
+  }
+  return worst;
+}
+
+extern "C" ckkt_status ckkt_iterate_host(ckkt_ctx* c, const double* w_val, const double* g_val, const double* h_val,
+                                         const double* sigma_x, const double* d_s, const double* delta_x,
+                                         const double* r1, const double* r2, const double* r3, const double* r4,
+                                         double* dx, double* ds, double* dy, double* dz, int32_t* not_pd,
+                                         ckkt_info* info) {
+  if (!c || !c->has_device) return CKKT_INVALID_ARG;
+  CK(cudaSetDevice(c->opt.device));
+  const int B = c->B;
+  const size_t Bn = (size_t)B * c->n, Bme = (size_t)B * c->me, Bmi = (size_t)B * c->mi;
+  if (!c->st_w) {
+    ckkt_status s;
+    if ((s = dalloc(c, (void**)&c->st_w, sizeof(double) * B * std::max<int64_t>(c->w_nnz, 1))) != CKKT_OK) return s;
+    if ((s = dalloc(c, (void**)&c->st_g, sizeof(double) * B * std::max<int64_t>(c->g_nnz, 1))) != CKKT_OK) return s;
+    if ((s = dalloc(c, (void**)&c->st_h, sizeof(double) * B * std::max<int64_t>(c->h_nnz, 1))) != CKKT_OK) return s;
+    if ((s = dalloc(c, (void**)&c->st_sig, sizeof(double) * Bn)) != CKKT_OK) return s;
+    if ((s = dalloc(c, (void**)&c->st_ds, sizeof(double) * std::max<size_t>(Bmi, 1))) != CKKT_OK) return s;
+    if ((s = dalloc(c, (void**)&c->st_del, sizeof(double) * B)) != CKKT_OK) return s;
+    if ((s = dalloc(c, (void**)&c->st_r1, sizeof(double) * Bn)) != CKKT_OK) return s;
+    if ((s = dalloc(c, (void**)&c->st_r2, sizeof(double) * std::max<size_t>(Bmi, 1))) != CKKT_OK) return s;
+    if ((s = dalloc(c, (void**)&c->st_r3, sizeof(double) * std::max<size_t>(Bme, 1))) != CKKT_OK) return s;
+    if ((s = dalloc(c, (void**)&c->st_r4, sizeof(double) * std::max<size_t>(Bmi, 1))) != CKKT_OK) return s;
+    if ((s = dalloc(c, (void**)&c->st_dx, sizeof(double) * Bn)) != CKKT_OK) return s;
+    if ((s = dalloc(c, (void**)&c->st_ds_o, sizeof(double) * std::max<size_t>(Bmi, 1))) != CKKT_OK) return s;
+    if ((s = dalloc(c, (void**)&c->st_dy, sizeof(double) * std::max<size_t>(Bme, 1))) != CKKT_OK) return s;
+    if ((s = dalloc(c, (void**)&c->st_dz, sizeof(double) * std::max<size_t>(Bmi, 1))) != CKKT_OK) return s;
+    if ((s = dalloc(c, (void**)&c->st_notpd, sizeof(int) * B)) != CKKT_OK) return s;
+  }
+  cudaStream_t st = c->stream;
+  auto h2d = [&](double* dst, const double* src, size_t cnt) -> cudaError_t {
+    if (!src || cnt == 0) return cudaSuccess;
+    return cudaMemcpyAsync(dst, src, sizeof(double) * cnt, cudaMemcpyHostToDevice, st);
+  };
+  CK(h2d(c->st_w, w_val, (size_t)B * c->w_nnz));
+  CK(h2d(c->st_g, g_val, (size_t)B * c->g_nnz));
+  CK(h2d(c->st_h, h_val, (size_t)B * c->h_nnz));
+  CK(h2d(c->st_sig, sigma_x, Bn));
+  CK(h2d(c->st_ds, d_s, Bmi));
+  CK(h2d(c->st_del, delta_x, B));
+  CK(h2d(c->st_r1, r1, Bn));
+  CK(h2d(c->st_r2, r2, Bmi));
+  CK(h2d(c->st_r3, r3, Bme));
+  CK(h2d(c->st_r4, r4, Bmi));
+  ckkt_status s = ckkt_refactor(c, c->st_w, c->st_g, c->st_h, c->st_sig, c->st_ds, delta_x ? c->st_del : nullptr,
+                                c->st_notpd, nullptr);
+  if (s != CKKT_OK) return s;
+  std::vector<ckkt_info> tmp(B);
+  s = ckkt_solve(c, c->st_r1, c->st_r2, c->st_r3, c->st_r4, c->st_dx, c->st_ds_o, c->st_dy, c->st_dz,
+                 info ? info : tmp.data());
+  auto d2h = [&](double* dst, const double* src, size_t cnt) -> cudaError_t {
+    if (!dst || cnt == 0) return cudaSuccess;
+    return cudaMemcpyAsync(dst, src, sizeof(double) * cnt, cudaMemcpyDeviceToHost, st);
+  };
+  CK(d2h(dx, c->st_dx, Bn));
+  CK(d2h(ds, c->st_ds_o, Bmi));
+  CK(d2h(dy, c->st_dy, Bme));
+  CK(d2h(dz, c->st_dz, Bmi));
+  if (not_pd) CK(cudaMemcpyAsync(not_pd, c->st_notpd, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return s;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Debug export (not part of include/ckkt.h): copies internal arrays to host memory.
+//   what: 0 = L storage (all instances), 1 = K values, 2 = perm2, 3 = sfirst, 4 = srowptr (int64),
+//         5 = srows, 6 = pofs (int64), 7 = kp (int64), 8 = ki
+// Returns the element count when host == NULL.
+// ---------------------------------------------------------------------------------------------
+extern "C" int64_t ckkt_debug_get(const ckkt_ctx* c, int what, void* host) {
+  if (!c) return -1;
+  const auto& A = c->A;
+  auto cp = [&](const void* src, size_t bytes, bool dev) -> void {
+    if (!host) return;
+    if (dev) cudaMemcpy(host, src, bytes, cudaMemcpyDeviceToHost);
+    else std::memcpy(host, src, bytes);
+  };
+  switch (what) {
+    case 0: cp(c->L, sizeof(double) * c->B * c->Lsize, true); return (int64_t)c->B * c->Lsize;
+    case 1: cp(c->Kval, sizeof(double) * c->B * c->nnzk, true); return (int64_t)c->B * c->nnzk;
+    case 2: cp(A.perm2.data(), 4 * A.perm2.size(), false); return A.perm2.size();
+    case 3: cp(A.sfirst.data(), 4 * A.sfirst.size(), false); return A.sfirst.size();
+    case 4: cp(A.srowptr.data(), 8 * A.srowptr.size(), false); return A.srowptr.size();
+    case 5: cp(A.srows.data(), 4 * A.srows.size(), false); return A.srows.size();
+    case 6: cp(A.pofs.data(), 8 * A.pofs.size(), false); return A.pofs.size();
+    case 7: cp(A.kp.data(), 8 * A.kp.size(), false); return A.kp.size();
+    case 8: cp(A.ki.data(), 4 * A.ki.size(), false); return A.ki.size();
+  }
+  return -1;
+}

@@ -1,0 +1,115 @@
+"""CPU checks of the C ABI: libckkt.so loads, exports every symbol include/ckkt.h declares, and its
+host-only symbolic analysis (device = -1) is bit-exact with the oracle's independent implementation."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from inputs import distillation as dist
+from inputs.random_kkt import random_instance
+from oracle import kkt as OK
+from paper_2403_15913_b200 import ckkt
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+E32 = np.zeros(1, np.int32)
+
+
+def _declared_symbols():
+    src = open(os.path.join(ROOT, "include", "ckkt.h")).read()
+    return sorted(set(re.findall(r"\b(ckkt_[a-z_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = ckkt.lib()
+    syms = _declared_symbols()
+    assert len(syms) >= 10
+    for s in syms:
+        assert hasattr(L, s), s
+    assert sorted(ckkt.EXPORTED) == syms
+
+
+def test_struct_layouts_match_header():
+    # sizes of the ABI structs (x86-64 SysV), cross-checked against offsets computed by ctypes
+    assert ctypes.sizeof(ckkt.ckkt_pattern) == 4 * 3 + 4 + 8 + 8 * 6
+    assert ctypes.sizeof(ckkt.ckkt_info) == 4 * 4 + 8 * 3
+    o = ckkt.default_options()
+    assert o.strategy == ckkt.CKKT_HYKKT and o.gamma == 1e7 and o.cg_rtol == 1e-10 and o.cg_maxit == 200
+    assert o.batch == 1 and o.ref_maxit == 10
+
+
+def _host_ctx(n, me, mi, w_row, w_col, g_rp, g_c, h_rp, h_c, **kw):
+    return ckkt.Context(n, me, mi, w_row, w_col, g_rp, g_c, h_rp, h_c, device=-1, **kw)
+
+
+@pytest.mark.parametrize("N,leaf", [(3, 16), (50, 64), (200, 268), (300, 1072)])
+def test_symbolic_bit_exact_distillation(N, leaf):
+    pat = dist.build_pattern(N)
+    ctx = _host_ctx(pat.n, pat.m, 0, pat.w_row, pat.w_col, pat.j_rowptr, pat.j_col, None, None, leaf=leaf)
+    perm, parent, cc, Lp, Li = ctx.export_symbolic()
+    o = OK.SparseKKT(pat.n, pat.m, 0, pat.w_row, pat.w_col, pat.j_rowptr, pat.j_col, E32, E32[:0], leaf=leaf)
+    assert np.array_equal(perm, o.perm)
+    assert np.array_equal(parent, o.parent)
+    assert np.array_equal(cc, o.colcount)
+    assert np.array_equal(Lp, o.Lp) and np.array_equal(Li, o.Li)
+    sz = ctx.get_sizes()
+    assert sz["nnz_l"] == len(o.Li) and sz["nnz_k"] == len(o.Ai)
+
+
+def test_symbolic_bit_exact_lifted_pattern_equals_hykkt_pattern():
+    """Lifted (rows in H) and HyKKT (rows in G) share the K pattern (SURVEY §8 note); same symbolic."""
+    pat = dist.build_pattern(30)
+    a = _host_ctx(pat.n, pat.m, 0, pat.w_row, pat.w_col, pat.j_rowptr, pat.j_col, None, None, leaf=128)
+    b = _host_ctx(pat.n, 0, pat.m, pat.w_row, pat.w_col, None, None, pat.j_rowptr, pat.j_col, leaf=128,
+                  strategy=ckkt.CKKT_LIFTED)
+    for x, y in zip(a.export_symbolic(), b.export_symbolic()):
+        assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_symbolic_bit_exact_random(seed):
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(5, 80))
+    me = int(rng.integers(0, n // 2))
+    mi = int(rng.integers(0, n))
+    inst = random_instance(n, me, mi, seed=seed, density=float(rng.uniform(0.03, 0.2)))
+    leaf = int(rng.integers(2, 20))
+    ctx = _host_ctx(n, me, mi, inst.w_row, inst.w_col, inst.g_rowptr, inst.g_col, inst.h_rowptr, inst.h_col,
+                    leaf=leaf)
+    perm, parent, cc, Lp, Li = ctx.export_symbolic()
+    o = OK.SparseKKT(n, me, mi, inst.w_row, inst.w_col, inst.g_rowptr, inst.g_col, inst.h_rowptr, inst.h_col,
+                     leaf=leaf)
+    assert np.array_equal(perm, o.perm) and np.array_equal(parent, o.parent)
+    assert np.array_equal(Lp, o.Lp) and np.array_equal(Li, o.Li)
+
+
+def test_caller_perm_is_used():
+    pat = dist.build_pattern(5)
+    perm = np.random.default_rng(0).permutation(pat.n).astype(np.int32)
+    ctx = _host_ctx(pat.n, pat.m, 0, pat.w_row, pat.w_col, pat.j_rowptr, pat.j_col, None, None, perm=perm)
+    p, parent, cc, Lp, Li = ctx.export_symbolic()
+    assert np.array_equal(p, perm)
+    o = OK.SparseKKT(pat.n, pat.m, 0, pat.w_row, pat.w_col, pat.j_rowptr, pat.j_col, E32, E32[:0], perm=perm)
+    assert np.array_equal(parent, o.parent) and np.array_equal(Li, o.Li)
+
+
+def test_pattern_errors():
+    with pytest.raises(ckkt.CKKTError) as e:
+        _host_ctx(3, 0, 0, np.array([0, 1]), np.array([1, 0]), None, None, None, None)  # upper entry
+    assert e.value.code == ckkt.CKKT_PATTERN_ERROR
+    with pytest.raises(ckkt.CKKTError) as e:
+        _host_ctx(3, 1, 0, np.array([0]), np.array([0]), np.array([0, 2]), np.array([2, 1]), None, None)  # unsorted
+    assert e.value.code == ckkt.CKKT_PATTERN_ERROR
+    with pytest.raises(ckkt.CKKTError) as e:  # Lifted with equality rows
+        _host_ctx(3, 1, 0, np.array([0]), np.array([0]), np.array([0, 1]), np.array([1]), None, None,
+                  strategy=ckkt.CKKT_LIFTED)
+    assert e.value.code == ckkt.CKKT_INVALID_ARG
+    with pytest.raises(ckkt.CKKTError) as e:
+        _host_ctx(3, 0, 0, np.array([0]), np.array([0]), None, None, None, None, perm=np.array([0, 0, 1]))
+    assert e.value.code == ckkt.CKKT_INVALID_ARG
+
+
+def test_device_calls_refuse_host_only_context():
+    ctx = _host_ctx(3, 0, 0, np.array([0, 1, 2]), np.array([0, 1, 2]), None, None, None, None)
+    assert ckkt.lib().ckkt_refactor(ctx.h, None, None, None, None, None, None, None, None) == ckkt.CKKT_INVALID_ARG

@@ -1,0 +1,98 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Bars (north_star): per block relative step error <= 1e-8, componentwise KKT backward
+error <= 1e-10, integer arrays bit-exact, NOT_PD flag identical, k_CG within +-1."""
+import numpy as np
+import pytest
+
+from kkt_cases import (block_errors, distillation_case, host_kaug_backward_error, random_case, run_gpu,
+                             run_oracle)
+
+pytestmark = pytest.mark.gpu
+
+STEP_TOL = 1e-8
+RES_TOL = 1e-10
+
+
+def _check(case, strategy, gamma=1e7, leaf=64, step_tol=STEP_TOL):
+    g = run_gpu(case, strategy, gamma=gamma, leaf=leaf)
+    for b in range(case.B):
+        o, d, info = run_oracle(case, b, strategy, gamma=gamma, leaf=leaf)
+        if d is None:
+            assert g["notpd"][b] == 1
+            continue
+        assert g["notpd"][b] == 0
+        if not info.cg_converged:
+            # out of contract (reading R6 cap): both sides must report CG non-convergence
+            assert g["info"][b]["status"] == 2 and g["info"][b]["k_cg"] == info.k_cg
+            continue
+        errs = block_errors(g, b, d)
+        assert max(errs) <= step_tol, (b, errs, g["info"][b], info)
+        gi = g["info"][b]
+        assert gi["rel_res"] <= RES_TOL, gi
+        assert abs(gi["k_cg"] - info.k_cg) <= 1, (gi, info)
+        got = (g["dx"][b], g["ds"][b], g["dy"][b], g["dz"][b])
+        assert host_kaug_backward_error(case, b, got) <= RES_TOL
+    return g
+
+
+@pytest.mark.parametrize("shape", [(30, 8, 6), (41, 0, 12), (25, 10, 0), (60, 20, 15), (1, 0, 0), (7, 3, 0)])
+@pytest.mark.parametrize("strategy", [0, 1])
+def test_random_instances(shape, strategy):
+    n, me, mi = shape
+    if strategy == 0 and me > 0:
+        pytest.skip("Lifted needs m_e = 0")
+    case = random_case(n, me, mi, seeds=[11, 12, 13], sigma_range=(1e-4, 1e4), d_range=(1e-2, 1e6))
+    _check(case, strategy, gamma=1e4 if strategy else 0.0, leaf=8)
+
+
+def test_random_wide_range_lifted():
+    case = random_case(40, 0, 20, seeds=[5, 6], d_range=(1e5, 1e12), sigma_range=(1e-8, 1e8))
+    _check(case, 0, leaf=16)
+
+
+@pytest.mark.parametrize("strategy", [0, 1])
+def test_distillation_c1(strategy):
+    """Config 1 (N=50), several iterates of the synthetic trajectory in one batch."""
+    case = distillation_case(50, strategy, iterates=[0, 5, 9, 13, 17])
+    _check(case, strategy)
+
+
+@pytest.mark.parametrize("leaf", [16, 268, 1072])
+def test_distillation_leaf_sizes(leaf):
+    case = distillation_case(60, 1, iterates=[2, 16])
+    _check(case, 1, leaf=leaf)
+
+
+def test_symbolic_bit_exact_on_device_context():
+    """perm, etree, column counts and L pattern exported by a device context equal the oracle."""
+    from oracle import kkt as OK
+    case = distillation_case(120, 1, iterates=[0])
+    g = run_gpu(case, 1, leaf=268)
+    perm, parent, cc, Lp, Li = g["ctx"].export_symbolic()
+    o = OK.SparseKKT(case.n, case.m_e, 0, case.w_row, case.w_col, case.g_rowptr, case.g_col,
+                     np.zeros(1, np.int32), np.zeros(0, np.int32), leaf=268)
+    assert np.array_equal(perm, o.perm) and np.array_equal(parent, o.parent)
+    assert np.array_equal(cc, o.colcount) and np.array_equal(Lp, o.Lp) and np.array_equal(Li, o.Li)
+
+
+def test_not_pd_flag_matches_oracle():
+    case = random_case(20, 0, 5, seeds=[3, 4, 5])
+    case.sigma_x[1] -= 1e3   # instance 1 indefinite
+    g = run_gpu(case, 0, leaf=8)
+    assert g["notpd"].tolist() == [0, 1, 0]
+    assert g["info"][1]["status"] == 1 and np.all(np.isnan(g["dx"][1]))
+    o, d, _ = run_oracle(case, 1, 0, leaf=8)
+    assert d is None
+    for b in (0, 2):
+        o, d, info = run_oracle(case, b, 0, leaf=8)
+        assert max(block_errors(g, b, d)) <= STEP_TOL
+
+
+def test_gamma_sweep_stress():
+    """Config 5: Sigma log-uniform over [1e-8, 1e8] on all variables, gamma in 1e4..1e8."""
+    case = distillation_case(40, 1, iterates=[12])
+    rng = np.random.default_rng(4000)
+    case.sigma_x[:] = np.exp(rng.uniform(np.log(1e-8), np.log(1e8), case.sigma_x.shape))
+    for gamma in (1e4, 1e5, 1e6, 1e7, 1e8):
+        _check(case, 1, gamma=gamma)
