@@ -7,18 +7,33 @@
 //   L pattern     = row-subtree traversal (rows of L_i* = the row subtree of i)
 //   supernodes    = fundamental supernodes of the postordered etree (internal, R11)
 //   maps          = K slot -> panel position, J^T D J product terms per slot,
-//                   left-looking update pairs with relative row maps, level schedule
+//                   multifrontal child lists with relative row maps, level schedule
 //
 // Independent of oracle/csrc (different algorithms and data structures).
 #include "analysis.h"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
 #include "../../include/ckkt.h"
 
 namespace ckkt {
+
+const AmalgamationParams& amalgamation_params() {
+  static AmalgamationParams P = [] {
+    AmalgamationParams p;
+    if (const char* e = getenv("CKKT_NRELAX")) {  // tuning experiments: "n0,n1,n2,z0,z1,z2,maxw" or "0"
+      if (std::string(e) == "0") p.enabled = false;
+      else sscanf(e, "%d,%d,%d,%lf,%lf,%lf,%d", &p.nrelax0, &p.nrelax1, &p.nrelax2, &p.zrelax0, &p.zrelax1,
+                  &p.zrelax2, &p.max_width);
+    }
+    return p;
+  }();
+  return P;
+}
 
 // ----------------------------------------------------------------------------
 // ordering
@@ -415,42 +430,113 @@ std::string analyze(const Pattern& p, int leaf, const int32_t* user_perm, Analys
     etree_liu(n, rp, rc, A.parent2);
     row_subtrees(n, rp, rc, A.parent2, A.colcount2, &Lp2, &Li2);
   }
-  // ---- fundamental supernodes
+  // ---- fundamental supernodes (fs*), then relaxed amalgamation into the internal supernodes
+  std::vector<int32_t> fsfirst, fsof(n), fsparent;
   {
     std::vector<int32_t> nchild(n, 0);
     for (int j = 0; j < n; ++j)
       if (A.parent2[j] >= 0) nchild[A.parent2[j]]++;
-    A.sfirst.clear();
-    A.snode_of.assign(n, 0);
     for (int j = 0; j < n; ++j) {
       bool merge = j > 0 && A.parent2[j - 1] == j && A.colcount2[j - 1] == A.colcount2[j] + 1 && nchild[j] == 1;
-      if (!merge) A.sfirst.push_back(j);
-      A.snode_of[j] = (int)A.sfirst.size() - 1;
+      if (!merge) fsfirst.push_back(j);
+      fsof[j] = (int)fsfirst.size() - 1;
     }
-    A.ns = (int)A.sfirst.size();
+    fsfirst.push_back(n);
+    const int nf = (int)fsfirst.size() - 1;
+    fsparent.assign(nf, -1);
+    for (int s = 0; s < nf; ++s) {
+      int last = fsfirst[s + 1] - 1;
+      if (A.parent2[last] >= 0) fsparent[s] = fsof[A.parent2[last]];
+    }
+  }
+  // Relaxed amalgamation (R11: internal storage only; padded entries are exact zeros).  In
+  // postorder the group ending right before supernode s is s's last child; it is merged into s
+  // when the merged panel stays narrow or gains few explicit zeros.
+  {
+    const int nf = (int)fsfirst.size() - 1;
+    std::vector<int32_t> gfirst, gtop;   // group first column, top fundamental supernode
+    std::vector<double> gzeros;
+    std::vector<int32_t> group_of_f(nf);
+    const AmalgamationParams& P = amalgamation_params();
+    for (int s = 0; s < nf; ++s) {
+      const int ws = fsfirst[s + 1] - fsfirst[s];
+      const int64_t ms = A.colcount2[fsfirst[s]];
+      bool merged = false;
+      if (!gfirst.empty() && P.enabled) {
+        int g = (int)gfirst.size() - 1;
+        int top = gtop[g];
+        if (fsparent[top] == s && fsfirst[top + 1] == fsfirst[s]) {
+          const int wg = fsfirst[s] - gfirst[g];
+          const int64_t mg = wg + (A.colcount2[fsfirst[top]] - (fsfirst[top + 1] - fsfirst[top]));  // rows of group
+          const int W = wg + ws;
+          const double newz = gzeros[g] + (double)wg * (double)(wg + ms - mg);
+          const double total = (double)W * (wg + ms) - (double)W * (W - 1) / 2.0;  // lower-trapezoid entries
+          const double frac = newz / total;
+          bool ok = W <= P.max_width &&
+                    (W <= P.nrelax0 || (W <= P.nrelax1 && frac < P.zrelax0) || (W <= P.nrelax2 && frac < P.zrelax1) ||
+                     frac < P.zrelax2);
+          if (ok) {
+            gtop[g] = s;
+            gzeros[g] = newz;
+            group_of_f[s] = g;
+            merged = true;
+          }
+        }
+      }
+      if (!merged) {
+        gfirst.push_back(fsfirst[s]);
+        gtop.push_back(s);
+        gzeros.push_back(0.0);
+        group_of_f[s] = (int)gfirst.size() - 1;
+      }
+    }
+    // final supernodes: groups split into chunks of at most MAXW columns (a chunk's rows are the
+    // suffix of the group's rows starting at its first column; chunk k's parent is chunk k+1)
+    constexpr int MAXW = 64;
+    std::vector<int32_t> sf, stopf;  // first column, top fundamental supernode of the owning group
+    for (size_t g = 0; g < gfirst.size(); ++g) {
+      const int gend = fsfirst[gtop[g] + 1];
+      for (int c0 = gfirst[g]; c0 < gend; c0 += MAXW) {
+        sf.push_back(c0);
+        stopf.push_back(gtop[g]);
+      }
+    }
+    A.ns = (int)sf.size();
+    A.sfirst = sf;
     A.sfirst.push_back(n);
+    A.snode_of.resize(n);
+    for (int s2 = 0; s2 < A.ns; ++s2)
+      for (int j = A.sfirst[s2]; j < A.sfirst[s2 + 1]; ++j) A.snode_of[j] = s2;
+    A.srowptr.assign(A.ns + 1, 0);
+    A.pofs.assign(A.ns + 1, 0);
+    for (int s2 = 0; s2 < A.ns; ++s2) {
+      const int top = stopf[s2];
+      const int w = A.sfirst[s2 + 1] - A.sfirst[s2];
+      const int64_t m = (int64_t)(fsfirst[top] - A.sfirst[s2]) + A.colcount2[fsfirst[top]];
+      A.srowptr[s2 + 1] = A.srowptr[s2] + m;
+      A.pofs[s2 + 1] = A.pofs[s2] + m * w;
+    }
+    A.srows.resize(A.srowptr[A.ns]);
+    for (int s2 = 0; s2 < A.ns; ++s2) {
+      const int top = stopf[s2];
+      int64_t o = A.srowptr[s2];
+      for (int j = A.sfirst[s2]; j < fsfirst[top]; ++j) A.srows[o++] = j;
+      if (A.sfirst[s2] <= fsfirst[top]) {
+        std::copy(Li2.begin() + Lp2[fsfirst[top]], Li2.begin() + Lp2[fsfirst[top] + 1], A.srows.begin() + o);
+      } else {  // chunk starting inside the top fundamental supernode: suffix of its structure
+        const int skip = A.sfirst[s2] - fsfirst[top];
+        std::copy(Li2.begin() + Lp2[fsfirst[top]] + skip, Li2.begin() + Lp2[fsfirst[top] + 1], A.srows.begin() + o);
+      }
+    }
+    A.sparent.assign(A.ns, -1);
+    for (int s2 = 0; s2 < A.ns; ++s2) {
+      const int last = A.sfirst[s2 + 1] - 1;
+      if (A.parent2[last] >= 0) A.sparent[s2] = A.snode_of[A.parent2[last]];
+    }
   }
   const int ns = A.ns;
-  A.srowptr.assign(ns + 1, 0);
-  A.pofs.assign(ns + 1, 0);
-  for (int s = 0; s < ns; ++s) {
-    int f = A.sfirst[s], w = A.sfirst[s + 1] - f;
-    int64_t m = A.colcount2[f];
-    A.srowptr[s + 1] = A.srowptr[s] + m;
-    A.pofs[s + 1] = A.pofs[s] + m * w;
-  }
-  A.srows.resize(A.srowptr[ns]);
-  for (int s = 0; s < ns; ++s) {
-    int f = A.sfirst[s];
-    std::copy(Li2.begin() + Lp2[f], Li2.begin() + Lp2[f + 1], A.srows.begin() + A.srowptr[s]);
-  }
   Li2.clear();
   Li2.shrink_to_fit();
-  A.sparent.assign(ns, -1);
-  for (int s = 0; s < ns; ++s) {
-    int last = A.sfirst[s + 1] - 1;
-    if (A.parent2[last] >= 0) A.sparent[s] = A.snode_of[A.parent2[last]];
-  }
   // levels (children before parents; postorder => child index < parent index)
   A.slevel.assign(ns, 0);
   for (int s = 0; s < ns; ++s)
@@ -465,52 +551,46 @@ std::string analyze(const Pattern& p, int leaf, const int32_t* user_perm, Analys
     std::vector<int32_t> nx(A.level_ptr.begin(), A.level_ptr.end() - 1);
     for (int s = 0; s < ns; ++s) A.level_list[nx[A.slevel[s]]++] = s;
   }
-  // ---- left-looking update pairs d -> s (d ascending per s)
+  // ---- multifrontal maps: children lists (ascending), relative positions of each supernode's
+  //      off-diagonal rows inside its parent's rows, update-matrix and update-vector offsets
   {
-    std::vector<std::vector<int32_t>> per_s_d(ns), per_s_p(ns), per_s_q(ns);
-    std::vector<std::vector<int64_t>> per_s_rel(ns);
-    A.relmap.clear();
-    for (int d = 0; d < ns; ++d) {
-      const int w = A.sfirst[d + 1] - A.sfirst[d];
-      const int64_t r0 = A.srowptr[d];
-      const int m = (int)(A.srowptr[d + 1] - r0);
-      int p = w;
-      while (p < m) {
-        int s = A.snode_of[A.srows[r0 + p]];
-        int q = p;
-        while (q < m && A.srows[r0 + q] < A.sfirst[s + 1]) ++q;
-        // relative positions of rows [p, m) of d inside srows[s]
-        int64_t rel = (int64_t)A.relmap.size();
-        const int32_t* sr = &A.srows[A.srowptr[s]];
-        const int ms = (int)(A.srowptr[s + 1] - A.srowptr[s]);
-        int t = 0;
-        for (int i = p; i < m; ++i) {
-          int row = A.srows[r0 + i];
-          while (t < ms && sr[t] < row) ++t;
-          if (t >= ms || sr[t] != row) { code = CKKT_PATTERN_ERROR; return "internal: row structure not nested"; }
-          A.relmap.push_back(t);
-        }
-        per_s_d[s].push_back(d);
-        per_s_p[s].push_back(p);
-        per_s_q[s].push_back(q);
-        per_s_rel[s].push_back(rel);
-        p = q;
+    A.ch_ptr.assign(ns + 1, 0);
+    for (int c = 0; c < ns; ++c)
+      if (A.sparent[c] >= 0) A.ch_ptr[A.sparent[c] + 1]++;
+    for (int s = 0; s < ns; ++s) A.ch_ptr[s + 1] += A.ch_ptr[s];
+    A.ch_list.resize(A.ch_ptr[ns]);
+    std::vector<int32_t> nx(A.ch_ptr.begin(), A.ch_ptr.end() - 1);
+    for (int c = 0; c < ns; ++c)
+      if (A.sparent[c] >= 0) A.ch_list[nx[A.sparent[c]]++] = c;
+    A.uofs.assign(ns + 1, 0);
+    A.vofs.assign(ns + 1, 0);
+    A.relofs.assign(ns + 1, 0);
+    for (int c = 0; c < ns; ++c) {
+      const int64_t m = A.srowptr[c + 1] - A.srowptr[c], w = A.sfirst[c + 1] - A.sfirst[c];
+      A.uofs[c + 1] = A.uofs[c] + (m - w) * (m - w);
+      A.vofs[c + 1] = A.vofs[c] + (m - w);
+      A.relofs[c + 1] = A.relofs[c] + (m - w);
+    }
+    A.relmap.resize(A.relofs[ns]);
+    for (int c = 0; c < ns; ++c) {
+      const int p = A.sparent[c];
+      const int w = A.sfirst[c + 1] - A.sfirst[c];
+      const int64_t r0 = A.srowptr[c];
+      const int m = (int)(A.srowptr[c + 1] - r0);
+      if (p < 0) {
+        if (m != w) { code = CKKT_PATTERN_ERROR; return "internal: root supernode with off-diagonal rows"; }
+        continue;
+      }
+      const int32_t* pr = &A.srows[A.srowptr[p]];
+      const int mp = (int)(A.srowptr[p + 1] - A.srowptr[p]);
+      int t = 0;
+      for (int i = w; i < m; ++i) {
+        const int row = A.srows[r0 + i];
+        while (t < mp && pr[t] < row) ++t;
+        if (t >= mp || pr[t] != row) { code = CKKT_PATTERN_ERROR; return "internal: row structure not nested"; }
+        A.relmap[A.relofs[c] + (i - w)] = t;
       }
     }
-    A.upd_ptr.assign(ns + 1, 0);
-    for (int s = 0; s < ns; ++s) A.upd_ptr[s + 1] = A.upd_ptr[s] + (int)per_s_d[s].size();
-    A.upd_d.resize(A.upd_ptr[ns]);
-    A.upd_p.resize(A.upd_ptr[ns]);
-    A.upd_q.resize(A.upd_ptr[ns]);
-    A.upd_rel.resize(A.upd_ptr[ns]);
-    for (int s = 0; s < ns; ++s)
-      for (size_t k = 0; k < per_s_d[s].size(); ++k) {
-        int64_t o = A.upd_ptr[s] + k;
-        A.upd_d[o] = per_s_d[s][k];
-        A.upd_p[o] = per_s_p[s][k];
-        A.upd_q[o] = per_s_q[s][k];
-        A.upd_rel[o] = per_s_rel[s][k];
-      }
   }
   // ---- condensation maps
   const int64_t nnzk = A.kp[n];

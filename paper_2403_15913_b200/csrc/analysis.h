@@ -40,9 +40,11 @@ struct Analysis {
   std::vector<int64_t> pofs;     // panel offsets (column-major m_s x w_s), [ns+1]
   int nlevels = 0;
   std::vector<int32_t> level_ptr, level_list;  // supernodes grouped by level (bottom-up)
-  // left-looking update pairs d -> s: for s, entries upd_ptr[s] .. upd_ptr[s+1]
-  std::vector<int32_t> upd_ptr, upd_d, upd_p, upd_q;
-  std::vector<int64_t> upd_rel;  // offset of the relative row map (rows [p, m_d) of d in srows[s])
+  // multifrontal structure: children of s = ch_list[ch_ptr[s] .. ch_ptr[s+1]) (ascending);
+  // relmap[relofs[c] + i] = position in srows[parent(c)] of the off-diagonal row w_c + i of c;
+  // update matrix U_c ((m_c-w_c)^2, column-major) at uofs[c]; update vector (m_c-w_c) at vofs[c]
+  std::vector<int32_t> ch_ptr, ch_list;
+  std::vector<int64_t> relofs, uofs, vofs;
   std::vector<int32_t> relmap;
   // condensation: per internal K slot k (CSC order)
   std::vector<int32_t> kmap;     // position inside the instance's panel storage
@@ -59,6 +61,16 @@ struct Analysis {
   // W entries mapped to internal order, for the residual SpMV (row2 >= col2 not guaranteed)
   std::vector<int32_t> w_row2, w_col2;
 };
+
+// Relaxed supernode amalgamation (CHOLMOD-style thresholds): merge when the merged width is
+// <= nrelax0, or <= nrelax1 with zero fraction < zrelax0, or <= nrelax2 with < zrelax1, or < zrelax2.
+struct AmalgamationParams {
+  bool enabled = true;
+  int nrelax0 = 4, nrelax1 = 16, nrelax2 = 48;
+  double zrelax0 = 0.8, zrelax1 = 0.1, zrelax2 = 0.05;
+  int max_width = 64;
+};
+const AmalgamationParams& amalgamation_params();
 
 // Returns "" on success, else an error message; code receives a ckkt_status value.
 std::string analyze(const Pattern& p, int leaf, const int32_t* user_perm, Analysis& A, int& code);

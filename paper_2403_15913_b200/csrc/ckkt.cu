@@ -3,8 +3,8 @@
 // Per-iteration path; every step runs in the kernels below:
 //   a1 k_condense        K_gamma values from W, Sigma_x, delta_x, J, D_s, gamma
 //   a2 k_rhs             r~ = r1 + H^T(D_s r4 - r2) [+ gamma G^T r3]
-//   a3 k_factor          supernodal left-looking Cholesky, level scheduled
-//   a4 k_fwd / k_bwd     supernodal triangular solves, level scheduled
+//   a3 k_factor_*        multifrontal supernodal Cholesky (DMMA SYRK), level sched.
+//   a4 k_fwd_* / k_bwd_* supernodal triangular solves, level scheduled
 //   a5 CG kernels        matrix-free CG on S_gamma = G K^{-1} G^T
 //   a6/a7 k_recover      dx un-permutation, ds = -r4 - H dx, dz = -r2 - D_s ds
 //   a8 k_kaug_residual   rho = -r - K_aug d and componentwise backward error        (R7)
@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <array>
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -35,6 +36,20 @@
   } while (0)
 
 static thread_local cudaError_t last_cuda_error = cudaSuccess;
+
+// CKKT_SYNC_DEBUG=1: synchronise and check after every launch, printing the failing kernel.
+static bool sync_debug() {
+  static int v = getenv("CKKT_SYNC_DEBUG") ? atoi(getenv("CKKT_SYNC_DEBUG")) : 0;
+  return v != 0;
+}
+#define DBG_SYNC(name)                                                                          \
+  do {                                                                                          \
+    if (sync_debug()) {                                                                         \
+      cudaError_t e_ = cudaDeviceSynchronize();                                                 \
+      if (e_ == cudaSuccess) e_ = cudaGetLastError();                                           \
+      if (e_ != cudaSuccess) fprintf(stderr, "ckkt: kernel %s failed: %s\n", name, cudaGetErrorString(e_)); \
+    }                                                                                           \
+  } while (0)
 
 namespace {
 
@@ -72,163 +87,7 @@ __global__ void k_condense(int64_t nnzk, const int64_t* __restrict__ wt_ptr, con
   Kval[b * nnzk + k] = acc;
 }
 
-struct SymDev {
-  const int32_t* sfirst;
-  const int64_t* srowptr;
-  const int32_t* srows;
-  const int64_t* pofs;
-  const int32_t* level_list;
-  const int32_t* upd_ptr;
-  const int32_t* upd_d;
-  const int32_t* upd_p;
-  const int32_t* upd_q;
-  const int64_t* upd_rel;
-  const int32_t* relmap;
-  const int64_t* kp;
-  const int32_t* kmap;
-  const int32_t* perm2;
-};
-
-// ------------------------------------------------------------------------------------------
-// a3: numeric factorization of the supernodes of one level (one CTA per supernode and instance).
-// Left-looking: the panel gathers the updates of every descendant d with rows in its columns,
-// then is factorized densely (Cholesky of the diagonal block + column scaling).
-// ------------------------------------------------------------------------------------------
-__global__ void k_factor(SymDev S, int lvl_off, double* __restrict__ L, int64_t Lsize,
-                         const double* __restrict__ Kval, int64_t nnzk, int* __restrict__ notpd,
-                         int* __restrict__ minpiv) {
-  const int s = S.level_list[lvl_off + blockIdx.x];
-  const int b = blockIdx.y;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  double* Lb = L + b * Lsize;
-  const double* Kb = Kval + b * nnzk;
-  const int f = S.sfirst[s], w = S.sfirst[s + 1] - f;
-  const int64_t r0 = S.srowptr[s];
-  const int m = (int)(S.srowptr[s + 1] - r0);
-  double* P = Lb + S.pofs[s];
-  for (int64_t i = tid; i < (int64_t)m * w; i += nt) P[i] = 0.0;
-  __syncthreads();
-  for (int64_t k = S.kp[f] + tid; k < S.kp[f + w]; k += nt) P[S.kmap[k]] = Kb[k];
-  __syncthreads();
-  for (int u = S.upd_ptr[s]; u < S.upd_ptr[s + 1]; ++u) {
-    const int d = S.upd_d[u], p = S.upd_p[u], q = S.upd_q[u];
-    const int32_t* rel = S.relmap + S.upd_rel[u];
-    const double* Pd = Lb + S.pofs[d];
-    const int md = (int)(S.srowptr[d + 1] - S.srowptr[d]);
-    const int wd = S.sfirst[d + 1] - S.sfirst[d];
-    const int32_t* rd = S.srows + S.srowptr[d];
-    const int nr = md - p, nc = q - p;
-    for (int e = tid; e < nr * nc; e += nt) {
-      const int i = e % nr, c = e / nr;
-      if (i < c) continue;
-      double t = 0.0;
-      for (int kk = 0; kk < wd; ++kk) t += Pd[p + i + (int64_t)kk * md] * Pd[p + c + (int64_t)kk * md];
-      P[rel[i] + (int64_t)(rd[p + c] - f) * m] -= t;
-    }
-    __syncthreads();
-  }
-  __shared__ double piv;
-  for (int j = 0; j < w; ++j) {
-    if (tid == 0) {
-      double dj = P[j + (int64_t)j * m];
-      if (!(dj > 0.0) || !isfinite(dj)) {
-        notpd[b] = 1;
-        atomicMin(&minpiv[b], f + j);
-        dj = nan("");
-      }
-      piv = sqrt(dj);
-      P[j + (int64_t)j * m] = piv;
-    }
-    __syncthreads();
-    const double pv = piv;
-    for (int i = j + 1 + tid; i < m; i += nt) P[i + (int64_t)j * m] /= pv;
-    __syncthreads();
-    const int nrest = w - j - 1;
-    for (int e = tid; e < nrest * m; e += nt) {
-      const int c = j + 1 + e / m, i = e % m;
-      if (i >= c) P[i + (int64_t)c * m] -= P[i + (int64_t)j * m] * P[c + (int64_t)j * m];
-    }
-    __syncthreads();
-  }
-}
-
-// ------------------------------------------------------------------------------------------
-// a4: forward substitution L y = x (in place, internal order) for the supernodes of one level.
-// ------------------------------------------------------------------------------------------
-__global__ void k_fwd(SymDev S, int lvl_off, const double* __restrict__ L, int64_t Lsize, double* __restrict__ X,
-                      int n, const int* __restrict__ skip) {
-  extern __shared__ double y[];
-  const int s = S.level_list[lvl_off + blockIdx.x];
-  const int b = blockIdx.y;
-  if (skip && skip[b]) return;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const double* Lb = L + b * Lsize;
-  double* x = X + (int64_t)b * n;
-  const int f = S.sfirst[s], w = S.sfirst[s + 1] - f;
-  const int m = (int)(S.srowptr[s + 1] - S.srowptr[s]);
-  const double* P = Lb + S.pofs[s];
-  for (int i = tid; i < w; i += nt) y[i] = x[f + i];
-  __syncthreads();
-  for (int u = S.upd_ptr[s]; u < S.upd_ptr[s + 1]; ++u) {
-    const int d = S.upd_d[u], p = S.upd_p[u], q = S.upd_q[u];
-    const double* Pd = Lb + S.pofs[d];
-    const int md = (int)(S.srowptr[d + 1] - S.srowptr[d]);
-    const int fd = S.sfirst[d], wd = S.sfirst[d + 1] - fd;
-    const int32_t* rd = S.srows + S.srowptr[d];
-    for (int c = p + tid; c < q; c += nt) {
-      double t = 0.0;
-      for (int kk = 0; kk < wd; ++kk) t += Pd[c + (int64_t)kk * md] * x[fd + kk];
-      y[rd[c] - f] -= t;
-    }
-    __syncthreads();
-  }
-  for (int j = 0; j < w; ++j) {
-    if (tid == 0) y[j] /= P[j + (int64_t)j * m];
-    __syncthreads();
-    const double yj = y[j];
-    for (int i = j + 1 + tid; i < w; i += nt) y[i] -= P[i + (int64_t)j * m] * yj;
-    __syncthreads();
-  }
-  for (int i = tid; i < w; i += nt) x[f + i] = y[i];
-}
-
-// backward substitution L^T x = y for the supernodes of one level (levels processed top-down)
-__global__ void k_bwd(SymDev S, int lvl_off, const double* __restrict__ L, int64_t Lsize, double* __restrict__ X,
-                      int n, const int* __restrict__ skip) {
-  extern __shared__ double y[];
-  __shared__ double red[TPB / 32];
-  const int s = S.level_list[lvl_off + blockIdx.x];
-  const int b = blockIdx.y;
-  if (skip && skip[b]) return;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const double* Lb = L + b * Lsize;
-  double* x = X + (int64_t)b * n;
-  const int f = S.sfirst[s], w = S.sfirst[s + 1] - f;
-  const int64_t r0 = S.srowptr[s];
-  const int m = (int)(S.srowptr[s + 1] - r0);
-  const double* P = Lb + S.pofs[s];
-  for (int c = tid; c < w; c += nt) {
-    double t = x[f + c];
-    for (int i = w; i < m; ++i) t -= P[i + (int64_t)c * m] * x[S.srows[r0 + i]];
-    y[c] = t;
-  }
-  __syncthreads();
-  for (int j = w - 1; j >= 0; --j) {
-    // y[j] = (y[j] - sum_{i>j} P[i,j] y[i]) / P[j,j]
-    double part = 0.0;
-    for (int i = j + 1 + tid; i < w; i += nt) part += P[i + (int64_t)j * m] * y[i];
-    for (int o = 16; o > 0; o >>= 1) part += __shfl_down_sync(0xffffffffu, part, o);
-    if ((tid & 31) == 0) red[tid >> 5] = part;
-    __syncthreads();
-    if (tid == 0) {
-      double tsum = 0.0;
-      for (int k = 0; k < nt / 32; ++k) tsum += red[k];
-      y[j] = (y[j] - tsum) / P[j + (int64_t)j * m];
-    }
-    __syncthreads();
-  }
-  for (int i = tid; i < w; i += nt) x[f + i] = y[i];
-}
+#include "mf_kernels.cuh"
 
 __global__ void k_init_flags(int B, int* notpd, int* minpiv) {
   int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -623,7 +482,12 @@ struct ckkt_ctx {
   int32_t *g_rowptr = nullptr, *g_col2 = nullptr, *h_rowptr = nullptr, *h_col2 = nullptr;
   int32_t *ws_ptr = nullptr, *ws_col = nullptr, *ws_idx = nullptr;
   // numeric
-  double *Kval = nullptr, *L = nullptr;
+  double *Kval = nullptr, *L = nullptr, *Ub = nullptr, *Vb = nullptr;
+  int64_t Usize = 0, Vsize = 0;
+  int max_m = 1;
+  std::vector<int32_t> lsmall_ptr, lbig_ptr;  // per level offsets into the small / big lists
+  int32_t *lsmall = nullptr, *lbig = nullptr;
+  int64_t big_smem = 0;
   int *notpd = nullptr, *minpiv = nullptr;
   // last refactor values (caller-owned, must stay valid until the next refactor)
   const double *w_val = nullptr, *g_val = nullptr, *h_val = nullptr, *sigma = nullptr, *d_s = nullptr,
@@ -678,23 +542,49 @@ ckkt_status setup_device(ckkt_ctx* c) {
     dst = upload(vec, o, by);                 \
     if (!dst) return CKKT_OUT_OF_MEMORY;      \
   } while (0)
-  int32_t *sfirst, *srows, *level_list, *upd_ptr, *upd_d, *upd_p, *upd_q, *relmap, *kmap, *perm2;
-  int64_t *srowptr, *pofs, *upd_rel, *kp;
+  int32_t *sfirst, *srows, *level_list, *ch_ptr, *ch_list, *relmap, *kmap, *perm2;
+  int64_t *srowptr, *pofs, *relofs, *uofs, *vofs, *kp;
   UP(sfirst, A.sfirst);
   UP(srowptr, A.srowptr);
   UP(srows, A.srows);
   UP(pofs, A.pofs);
   UP(level_list, A.level_list);
-  UP(upd_ptr, A.upd_ptr);
-  UP(upd_d, A.upd_d);
-  UP(upd_p, A.upd_p);
-  UP(upd_q, A.upd_q);
-  UP(upd_rel, A.upd_rel);
+  UP(ch_ptr, A.ch_ptr);
+  UP(ch_list, A.ch_list);
+  UP(relofs, A.relofs);
   UP(relmap, A.relmap);
+  UP(uofs, A.uofs);
+  UP(vofs, A.vofs);
   UP(kp, A.kp);
   UP(kmap, A.kmap);
   UP(perm2, A.perm2);
-  c->S = SymDev{sfirst, srowptr, srows, pofs, level_list, upd_ptr, upd_d, upd_p, upd_q, upd_rel, relmap, kp, kmap, perm2};
+  c->S = SymDev{sfirst, srowptr, srows, pofs, level_list, ch_ptr, ch_list, relofs, relmap, uofs, vofs, kp, kmap, perm2};
+  {  // split every level into small supernodes (one warp each) and big ones (one CTA each)
+    std::vector<int32_t> sm_list, bg_list;
+    c->lsmall_ptr.assign(1, 0);
+    c->lbig_ptr.assign(1, 0);
+    c->big_smem = 0;
+    for (int l = 0; l < A.nlevels; ++l) {
+      for (int k = A.level_ptr[l]; k < A.level_ptr[l + 1]; ++k) {
+        const int s = A.level_list[k];
+        const int64_t m = A.srowptr[s + 1] - A.srowptr[s], w = A.sfirst[s + 1] - A.sfirst[s];
+        if (m * w <= SMALL_PANEL && w <= 32) {
+          sm_list.push_back(s);
+        } else {
+          bg_list.push_back(s);
+          const int64_t mp = (m + 7) & ~7, wp = (w + 3) & ~3;
+          c->big_smem = std::max<int64_t>(c->big_smem, 8 * (mp * wp + 8));
+        }
+      }
+      c->lsmall_ptr.push_back((int32_t)sm_list.size());
+      c->lbig_ptr.push_back((int32_t)bg_list.size());
+    }
+    UP(c->lsmall, sm_list);
+    UP(c->lbig, bg_list);
+    if (c->big_smem > 227 * 1024) return CKKT_INVALID_ARG;
+    if (c->big_smem > 48 * 1024)
+      CK(cudaFuncSetAttribute(k_factor_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->big_smem));
+  }
   UP(c->wt_ptr, A.wt_ptr);
   UP(c->wt_idx, A.wt_idx);
   UP(c->jt_ptr, A.jt_ptr);
@@ -737,6 +627,8 @@ ckkt_status setup_device(ckkt_ctx* c) {
 #undef UP
   DALLOC(c->Kval, (size_t)B * c->nnzk);
   DALLOC(c->L, (size_t)B * c->Lsize);
+  DALLOC(c->Ub, (size_t)B * c->Usize);
+  DALLOC(c->Vb, (size_t)B * c->Vsize);
   DALLOC(c->notpd, B);
   DALLOC(c->minpiv, B);
   const size_t Bn = (size_t)B * n, Bme = (size_t)B * std::max(me, 1), Bmi = (size_t)B * std::max(mi, 1);
@@ -878,8 +770,13 @@ ckkt_status ckkt_setup(const ckkt_pattern* p, const ckkt_options* opt, ckkt_ctx*
   c->w_nnz = p->w_nnz;
   c->g_nnz = c->A.pat.g_rowptr.back();
   c->h_nnz = c->A.pat.h_rowptr.back();
-  for (int s = 0; s < c->A.ns; ++s) c->max_w = std::max(c->max_w, c->A.sfirst[s + 1] - c->A.sfirst[s]);
-  if (c->max_w * 8 > 48 * 1024) return CKKT_INVALID_ARG;
+  for (int s = 0; s < c->A.ns; ++s) {
+    c->max_w = std::max(c->max_w, c->A.sfirst[s + 1] - c->A.sfirst[s]);
+    c->max_m = std::max(c->max_m, (int)(c->A.srowptr[s + 1] - c->A.srowptr[s]));
+  }
+  if ((int64_t)SMALL_WARPS * (c->max_m + 32) * 8 > 48 * 1024) return CKKT_INVALID_ARG;
+  c->Usize = c->A.uofs[c->A.ns];
+  c->Vsize = c->A.vofs[c->A.ns];
   if (o.device >= 0) {
     c->has_device = true;
     ckkt_status st = setup_device(c.get());
@@ -949,13 +846,25 @@ ckkt_status ckkt_refactor(ckkt_ctx* c, const double* w_val, const double* g_val,
                                                      c->jt_r, c->kdiag, w_val, c->w_nnz, g_val, c->g_nnz, h_val,
                                                      c->h_nnz, sigma_x, d_s, delta_x, gamma, c->n, c->me, c->mi,
                                                      c->Kval);
+  DBG_SYNC("k_condense");
   c->launches += 2;
   const auto& A = c->A;
   for (int l = 0; l < A.nlevels; ++l) {
-    int cnt = A.level_ptr[l + 1] - A.level_ptr[l];
-    k_factor<<<dim3(cnt, B), 128, 0, st>>>(c->S, A.level_ptr[l], c->L, c->Lsize, c->Kval, c->nnzk, c->notpd,
-                                           c->minpiv);
-    c->launches++;
+    const int ns_ = c->lsmall_ptr[l + 1] - c->lsmall_ptr[l], nb_ = c->lbig_ptr[l + 1] - c->lbig_ptr[l];
+    if (ns_ > 0) {
+      k_factor_small<<<dim3((ns_ + SMALL_WARPS - 1) / SMALL_WARPS, B), 32 * SMALL_WARPS, 0, st>>>(
+          c->S, c->lsmall + c->lsmall_ptr[l], ns_, c->L, c->Lsize, c->Ub, c->Usize, c->Kval, c->nnzk, c->notpd,
+          c->minpiv);
+      DBG_SYNC("k_factor_small");
+      c->launches++;
+    }
+    if (nb_ > 0) {
+      k_factor_big<<<dim3(nb_, B), BIG_THREADS, c->big_smem, st>>>(c->S, c->lbig + c->lbig_ptr[l], c->L, c->Lsize,
+                                                                   c->Ub, c->Usize, c->Kval, c->nnzk, c->notpd,
+                                                                   c->minpiv);
+      DBG_SYNC("k_factor_big");
+      c->launches++;
+    }
   }
   k_final_flags<<<nblk(B), TPB, 0, st>>>(B, c->notpd, c->minpiv, c->S.perm2, not_pd, min_bad_pivot);
   c->launches++;
@@ -972,16 +881,30 @@ namespace {
 void ksolve(ckkt_ctx* c, double* x, const int* skip) {
   const auto& A = c->A;
   cudaStream_t st = c->stream;
-  const size_t sm = sizeof(double) * c->max_w;
+  const size_t sms = sizeof(double) * SMALL_WARPS * (c->max_m + 32);
+  const size_t smb = sizeof(double) * (c->max_m + 64);
   for (int l = 0; l < A.nlevels; ++l) {
-    int cnt = A.level_ptr[l + 1] - A.level_ptr[l];
-    k_fwd<<<dim3(cnt, c->B), 128, sm, st>>>(c->S, A.level_ptr[l], c->L, c->Lsize, x, c->n, skip);
+    const int ns_ = c->lsmall_ptr[l + 1] - c->lsmall_ptr[l], nb_ = c->lbig_ptr[l + 1] - c->lbig_ptr[l];
+    if (ns_ > 0)
+      k_fwd_small<<<dim3((ns_ + SMALL_WARPS - 1) / SMALL_WARPS, c->B), 32 * SMALL_WARPS, sms, st>>>(
+          c->S, c->lsmall + c->lsmall_ptr[l], ns_, c->L, c->Lsize, x, c->n, c->Vb, c->Vsize, c->max_m, skip);
+    if (nb_ > 0)
+      k_fwd_big<<<dim3(nb_, c->B), BIG_THREADS, smb, st>>>(c->S, c->lbig + c->lbig_ptr[l], c->L, c->Lsize, x, c->n,
+                                                            c->Vb, c->Vsize, skip);
   }
   for (int l = A.nlevels - 1; l >= 0; --l) {
-    int cnt = A.level_ptr[l + 1] - A.level_ptr[l];
-    k_bwd<<<dim3(cnt, c->B), TPB, sm, st>>>(c->S, A.level_ptr[l], c->L, c->Lsize, x, c->n, skip);
+    const int ns_ = c->lsmall_ptr[l + 1] - c->lsmall_ptr[l], nb_ = c->lbig_ptr[l + 1] - c->lbig_ptr[l];
+    if (nb_ > 0)
+      k_bwd_big<<<dim3(nb_, c->B), BIG_THREADS, smb, st>>>(c->S, c->lbig + c->lbig_ptr[l], c->L, c->Lsize, x, c->n,
+                                                            skip);
+    if (ns_ > 0)
+      k_bwd_small<<<dim3((ns_ + SMALL_WARPS - 1) / SMALL_WARPS, c->B), 32 * SMALL_WARPS, sms, st>>>(
+          c->S, c->lsmall + c->lsmall_ptr[l], ns_, c->L, c->Lsize, x, c->n, c->max_m, skip);
   }
-  c->launches += 2 * A.nlevels;
+  int64_t nl = 0;
+  for (int l = 0; l < A.nlevels; ++l)
+    nl += (c->lsmall_ptr[l + 1] > c->lsmall_ptr[l]) + (c->lbig_ptr[l + 1] > c->lbig_ptr[l]);
+  c->launches += 2 * nl;
 }
 
 void dot(ckkt_ctx* c, int64_t len, const double* a, const double* b, const int* skip) {
@@ -1278,6 +1201,8 @@ extern "C" ckkt_status ckkt_iterate_host(ckkt_ctx* c, const double* w_val, const
 //         5 = srows, 6 = pofs (int64), 7 = kp (int64), 8 = ki
 // Returns the element count when host == NULL.
 // ---------------------------------------------------------------------------------------------
+extern "C" const char* ckkt_debug_error_string() { return cudaGetErrorString(last_cuda_error); }
+
 extern "C" int64_t ckkt_debug_get(const ckkt_ctx* c, int what, void* host) {
   if (!c) return -1;
   const auto& A = c->A;
@@ -1296,6 +1221,20 @@ extern "C" int64_t ckkt_debug_get(const ckkt_ctx* c, int what, void* host) {
     case 6: cp(A.pofs.data(), 8 * A.pofs.size(), false); return A.pofs.size();
     case 7: cp(A.kp.data(), 8 * A.kp.size(), false); return A.kp.size();
     case 8: cp(A.ki.data(), 4 * A.ki.size(), false); return A.ki.size();
+    case 9: cp(A.ch_ptr.data(), 4 * A.ch_ptr.size(), false); return A.ch_ptr.size();
+    case 10: cp(A.ch_list.data(), 4 * A.ch_list.size(), false); return A.ch_list.size();
+    case 11: cp(A.relofs.data(), 8 * A.relofs.size(), false); return A.relofs.size();
+    case 12: cp(A.relmap.data(), 4 * A.relmap.size(), false); return A.relmap.size();
+    case 13: cp(A.uofs.data(), 8 * A.uofs.size(), false); return A.uofs.size();
+    case 14: cp(c->Ub, sizeof(double) * c->B * c->Usize, true); return (int64_t)c->B * c->Usize;
+    case 15: cp(A.kmap.data(), 4 * A.kmap.size(), false); return A.kmap.size();
+    case 16: cp(A.wt_ptr.data(), 8 * A.wt_ptr.size(), false); return A.wt_ptr.size();
+    case 17: cp(A.wt_idx.data(), 4 * A.wt_idx.size(), false); return A.wt_idx.size();
+    case 18: cp(A.jt_ptr.data(), 8 * A.jt_ptr.size(), false); return A.jt_ptr.size();
+    case 19: cp(A.jt_a.data(), 4 * A.jt_a.size(), false); return A.jt_a.size();
+    case 20: cp(A.jt_b.data(), 4 * A.jt_b.size(), false); return A.jt_b.size();
+    case 21: cp(A.jt_r.data(), 4 * A.jt_r.size(), false); return A.jt_r.size();
+    case 22: cp(A.dslot.data(), 4 * A.dslot.size(), false); return A.dslot.size();
   }
   return -1;
 }
