@@ -213,7 +213,9 @@ def run_ckkt(args, world, rank, local):
         torch.cuda.synchronize()
         lifted = {"ms_per_iter": ev0.elapsed_time(ev1) / args.steps,
                   "n_ref_mean": float(np.mean([i["n_ref"] for i in linfo])),
-                  "rel_res_max": float(max(i["rel_res"] for i in linfo))}
+                  "rel_res_max": float(max(i["rel_res"] for i in linfo)),
+                  "rel_res_unrefined_max": float(max(i["rel_res_unrefined"] for i in linfo)),
+                  "status_max": int(max(i["status"] for i in linfo))}
         ctxl.close()
     # e2e through the public host API (pinned host buffers)
     e2e = None
@@ -263,6 +265,7 @@ def run_ckkt(args, world, rank, local):
     if not args.no_cpu_baseline and world == 1:
         cpu = cpu_baseline(data, args)
     info_summary = {"k_cg_mean": float(np.mean([i["k_cg"] for i in infos])),
+                    "rel_res_unrefined_max": float(max(i["rel_res_unrefined"] for i in infos)),
                     "n_ref_mean": float(np.mean([i["n_ref"] for i in infos])),
                     "rel_res_max": float(max(i["rel_res"] for i in infos)),
                     "status_max": int(max(i["status"] for i in infos))}

@@ -485,9 +485,13 @@ struct ckkt_ctx {
   double *Kval = nullptr, *L = nullptr, *Ub = nullptr, *Vb = nullptr;
   int64_t Usize = 0, Vsize = 0;
   int max_m = 1;
-  std::vector<int32_t> lsmall_ptr, lbig_ptr;  // per level offsets into the small / big lists
-  int32_t *lsmall = nullptr, *lbig = nullptr;
-  int64_t big_smem = 0;
+  int ntask = 0, grid_fac = 1, grid_fwd = 1, grid_bwd = 1;
+  int epoch_fac = 0, epoch_fwd = 0, epoch_bwd = 0;
+  Sched Qfac{}, Qfwd{}, Qbwd{};
+  int nchunk = 0, nq = 0, nsub = 0;
+  int32_t *chunk_ptr = nullptr, *queue = nullptr, *sub_ptr = nullptr, *sub_nodes = nullptr;
+  int8_t* tinyflag = nullptr;
+  int64_t big_smem = 0, fac_smem = 0, sol_smem = 0;
   int *notpd = nullptr, *minpiv = nullptr;
   // last refactor values (caller-owned, must stay valid until the next refactor)
   const double *w_val = nullptr, *g_val = nullptr, *h_val = nullptr, *sigma = nullptr, *d_s = nullptr,
@@ -542,7 +546,7 @@ ckkt_status setup_device(ckkt_ctx* c) {
     dst = upload(vec, o, by);                 \
     if (!dst) return CKKT_OUT_OF_MEMORY;      \
   } while (0)
-  int32_t *sfirst, *srows, *level_list, *ch_ptr, *ch_list, *relmap, *kmap, *perm2;
+  int32_t *sfirst, *srows, *level_list, *ch_ptr, *ch_list, *relmap, *kmap, *perm2, *sparent;
   int64_t *srowptr, *pofs, *relofs, *uofs, *vofs, *kp;
   UP(sfirst, A.sfirst);
   UP(srowptr, A.srowptr);
@@ -558,32 +562,118 @@ ckkt_status setup_device(ckkt_ctx* c) {
   UP(kp, A.kp);
   UP(kmap, A.kmap);
   UP(perm2, A.perm2);
-  c->S = SymDev{sfirst, srowptr, srows, pofs, level_list, ch_ptr, ch_list, relofs, relmap, uofs, vofs, kp, kmap, perm2};
-  {  // split every level into small supernodes (one warp each) and big ones (one CTA each)
-    std::vector<int32_t> sm_list, bg_list;
-    c->lsmall_ptr.assign(1, 0);
-    c->lbig_ptr.assign(1, 0);
+  UP(sparent, A.sparent);
+  c->S = SymDev{sfirst, srowptr, srows, pofs, level_list, ch_ptr, ch_list, relofs, relmap, uofs, vofs, kp, kmap, perm2,
+                sparent};
+  {  // persistent-kernel tasks in level order: big supernodes (one CTA) and bundles of small ones (one warp each)
+    std::vector<int32_t> tsn, tbig;
     c->big_smem = 0;
     for (int l = 0; l < A.nlevels; ++l) {
+      std::vector<int32_t> small;
       for (int k = A.level_ptr[l]; k < A.level_ptr[l + 1]; ++k) {
         const int s = A.level_list[k];
         const int64_t m = A.srowptr[s + 1] - A.srowptr[s], w = A.sfirst[s + 1] - A.sfirst[s];
         if (m * w <= SMALL_PANEL && w <= 32) {
-          sm_list.push_back(s);
+          small.push_back(s);
         } else {
-          bg_list.push_back(s);
+          tbig.push_back(1);
+          tsn.push_back(s);
+          for (int q = 1; q < SMALL_WARPS; ++q) tsn.push_back(-1);
           const int64_t mp = (m + 7) & ~7, wp = (w + 3) & ~3;
           c->big_smem = std::max<int64_t>(c->big_smem, 8 * (mp * wp + 8));
         }
       }
-      c->lsmall_ptr.push_back((int32_t)sm_list.size());
-      c->lbig_ptr.push_back((int32_t)bg_list.size());
+      for (size_t k = 0; k < small.size(); k += SMALL_WARPS) {
+        tbig.push_back(0);
+        for (int q = 0; q < SMALL_WARPS; ++q) tsn.push_back(k + q < small.size() ? small[k + q] : -1);
+      }
     }
-    UP(c->lsmall, sm_list);
-    UP(c->lbig, bg_list);
-    if (c->big_smem > 227 * 1024) return CKKT_INVALID_ARG;
-    if (c->big_smem > 48 * 1024)
-      CK(cudaFuncSetAttribute(k_factor_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->big_smem));
+    c->ntask = (int)tbig.size();
+    int32_t *d_tsn, *d_tbig;
+    UP(d_tsn, tsn);
+    UP(d_tbig, tbig);
+    std::vector<int32_t> zeros((size_t)B * A.ns, 0), z2(2, 0);
+    int32_t *dfac, *dfwd, *dbwd, *cfac, *cfwd, *cbwd;
+    UP(dfac, zeros);
+    UP(dfwd, zeros);
+    UP(dbwd, zeros);
+    UP(cfac, z2);
+    UP(cfwd, z2);
+    UP(cbwd, z2);
+    c->Qfac = Sched{c->ntask, d_tsn, d_tbig, dfac, cfac};
+    c->Qfwd = Sched{c->ntask, d_tsn, d_tbig, dfwd, cfwd};
+    c->Qbwd = Sched{c->ntask, d_tsn, d_tbig, dbwd, cbwd};
+    c->fac_smem = std::max<int64_t>(c->big_smem, 8 * SMALL_WARPS * SMALL_PANEL);
+    c->sol_smem = 8 * SOLVE_WARPS * (c->max_m + 64 + 32 * 33);
+    if (c->fac_smem > 227 * 1024 || c->sol_smem > 227 * 1024) return CKKT_INVALID_ARG;
+    CK(cudaFuncSetAttribute(k_factor_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->fac_smem));
+    CK(cudaFuncSetAttribute(k_fwd_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->sol_smem));
+    CK(cudaFuncSetAttribute(k_bwd_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->sol_smem));
+    int dev_sms = 0, occ = 0;
+    CK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->opt.device));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_factor_persist, MF_THREADS, c->fac_smem));
+    c->grid_fac = std::max(1, std::min(occ * dev_sms, c->ntask * B));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fwd_persist, 32 * SOLVE_WARPS, c->sol_smem));
+    c->grid_fwd = std::max(1, std::min(occ * dev_sms, (A.ns * B + SOLVE_WARPS - 1) / SOLVE_WARPS));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bwd_persist, 32 * SOLVE_WARPS, c->sol_smem));
+    c->grid_bwd = std::max(1, std::min(occ * dev_sms, (A.ns * B + SOLVE_WARPS - 1) / SOLVE_WARPS));
+    {  // tiny subtrees (one thread each) and the queue of the remaining supernodes (one warp each)
+      const int ns = A.ns;
+      std::vector<int8_t> T(ns, 0);
+      for (int s = 0; s < ns; ++s) {  // postorder: children before parents
+        const int64_t m = A.srowptr[s + 1] - A.srowptr[s], w = A.sfirst[s + 1] - A.sfirst[s];
+        bool t = m <= TINY_M && w <= TINY_W;
+        for (int ci = A.ch_ptr[s]; t && ci < A.ch_ptr[s + 1]; ++ci) t = T[A.ch_list[ci]] != 0;
+        T[s] = t;
+      }
+      std::vector<std::vector<int32_t>> subs;
+      std::vector<int32_t> stack;
+      for (int s = 0; s < ns; ++s) {
+        if (!T[s] || (A.sparent[s] >= 0 && T[A.sparent[s]])) continue;
+        std::vector<int32_t> nodes;  // postorder of the subtree rooted at s
+        std::vector<std::pair<int, int>> st{{s, A.ch_ptr[s]}};
+        while (!st.empty()) {
+          auto& top = st.back();
+          if (top.second < A.ch_ptr[top.first + 1]) {
+            const int c = A.ch_list[top.second++];
+            st.push_back({c, A.ch_ptr[c]});
+          } else {
+            nodes.push_back(top.first);
+            st.pop_back();
+          }
+        }
+        subs.push_back(std::move(nodes));
+      }
+      std::stable_sort(subs.begin(), subs.end(),
+                       [](const std::vector<int32_t>& a, const std::vector<int32_t>& b) { return a.size() > b.size(); });
+      std::vector<int32_t> sp{0}, sn;
+      for (auto& v : subs) {
+        sn.insert(sn.end(), v.begin(), v.end());
+        sp.push_back((int32_t)sn.size());
+      }
+      c->nsub = (int)subs.size();
+      c->sub_ptr = upload(sp, o, by);
+      c->sub_nodes = upload(sn, o, by);
+      c->tinyflag = upload(T, o, by);
+      std::vector<int32_t> q, lp{0};
+      for (int l = 0; l < A.nlevels; ++l) {
+        for (int k = A.level_ptr[l]; k < A.level_ptr[l + 1]; ++k)
+          if (!T[A.level_list[k]]) q.push_back(A.level_list[k]);
+        lp.push_back((int32_t)q.size());
+      }
+      c->nq = (int)q.size();
+      c->queue = upload(q, o, by);
+      const int64_t warps = (int64_t)c->grid_fwd * SOLVE_WARPS;
+      std::vector<int32_t> cp{0};
+      for (int l = 0; l < A.nlevels; ++l) {
+        const int64_t K = lp[l + 1] - lp[l];
+        const int csz = (int)std::max<int64_t>(1, std::min<int64_t>(16, (K * B) / (4 * warps)));
+        for (int64_t k = lp[l]; k < lp[l + 1]; k += csz) cp.push_back((int32_t)std::min<int64_t>(k + csz, lp[l + 1]));
+      }
+      c->nchunk = (int)cp.size() - 1;
+      c->chunk_ptr = upload(cp, o, by);
+      if (!c->chunk_ptr || !c->queue || !c->tinyflag || !c->sub_ptr || !c->sub_nodes) return CKKT_OUT_OF_MEMORY;
+    }
   }
   UP(c->wt_ptr, A.wt_ptr);
   UP(c->wt_idx, A.wt_idx);
@@ -774,7 +864,6 @@ ckkt_status ckkt_setup(const ckkt_pattern* p, const ckkt_options* opt, ckkt_ctx*
     c->max_w = std::max(c->max_w, c->A.sfirst[s + 1] - c->A.sfirst[s]);
     c->max_m = std::max(c->max_m, (int)(c->A.srowptr[s + 1] - c->A.srowptr[s]));
   }
-  if ((int64_t)SMALL_WARPS * (c->max_m + 32) * 8 > 48 * 1024) return CKKT_INVALID_ARG;
   c->Usize = c->A.uofs[c->A.ns];
   c->Vsize = c->A.vofs[c->A.ns];
   if (o.device >= 0) {
@@ -849,23 +938,12 @@ ckkt_status ckkt_refactor(ckkt_ctx* c, const double* w_val, const double* g_val,
   DBG_SYNC("k_condense");
   c->launches += 2;
   const auto& A = c->A;
-  for (int l = 0; l < A.nlevels; ++l) {
-    const int ns_ = c->lsmall_ptr[l + 1] - c->lsmall_ptr[l], nb_ = c->lbig_ptr[l + 1] - c->lbig_ptr[l];
-    if (ns_ > 0) {
-      k_factor_small<<<dim3((ns_ + SMALL_WARPS - 1) / SMALL_WARPS, B), 32 * SMALL_WARPS, 0, st>>>(
-          c->S, c->lsmall + c->lsmall_ptr[l], ns_, c->L, c->Lsize, c->Ub, c->Usize, c->Kval, c->nnzk, c->notpd,
-          c->minpiv);
-      DBG_SYNC("k_factor_small");
-      c->launches++;
-    }
-    if (nb_ > 0) {
-      k_factor_big<<<dim3(nb_, B), BIG_THREADS, c->big_smem, st>>>(c->S, c->lbig + c->lbig_ptr[l], c->L, c->Lsize,
-                                                                   c->Ub, c->Usize, c->Kval, c->nnzk, c->notpd,
-                                                                   c->minpiv);
-      DBG_SYNC("k_factor_big");
-      c->launches++;
-    }
-  }
+  ++c->epoch_fac;
+  k_factor_persist<<<c->grid_fac, MF_THREADS, c->fac_smem, st>>>(c->S, c->Qfac, A.ns, B, c->epoch_fac, c->L, c->Lsize,
+                                                                 c->Ub, c->Usize, c->Kval, c->nnzk, c->notpd,
+                                                                 c->minpiv);
+  DBG_SYNC("k_factor_persist");
+  c->launches++;
   k_final_flags<<<nblk(B), TPB, 0, st>>>(B, c->notpd, c->minpiv, c->S.perm2, not_pd, min_bad_pivot);
   c->launches++;
   CK(cudaGetLastError());
@@ -877,34 +955,44 @@ ckkt_status ckkt_refactor(ckkt_ctx* c, const double* w_val, const double* g_val,
 
 namespace {
 
+void launch_fwd(ckkt_ctx* c, double* x, const int* skip) {
+  cudaStream_t st = c->stream;
+  if (c->nsub > 0)
+    k_fwd_tiny<<<(c->nsub * c->B + 255) / 256, 256, 0, st>>>(c->S, c->sub_ptr, c->sub_nodes, c->nsub, c->B, c->L,
+                                                              c->Lsize, x, c->n, c->Vb, c->Vsize, skip);
+  DBG_SYNC("k_fwd_tiny");
+  ++c->epoch_fwd;
+  if (c->nq > 0)
+    k_fwd_persist<<<c->grid_fwd, 32 * SOLVE_WARPS, c->sol_smem, st>>>(c->S, c->queue, c->chunk_ptr, c->nchunk,
+                                                                       c->A.ns, c->Qfwd.ctr, c->Qfwd.done, c->B,
+                                                                       c->epoch_fwd, c->L, c->Lsize, x, c->n, c->Vb,
+                                                                       c->Vsize, c->max_m, skip, c->tinyflag);
+  DBG_SYNC("k_fwd_persist");
+}
+
+void launch_bwd(ckkt_ctx* c, double* x, const int* skip) {
+  cudaStream_t st = c->stream;
+  ++c->epoch_bwd;
+  if (c->nq > 0)
+    k_bwd_persist<<<c->grid_bwd, 32 * SOLVE_WARPS, c->sol_smem, st>>>(c->S, c->queue, c->chunk_ptr, c->nchunk,
+                                                                       c->A.ns, c->Qbwd.ctr, c->Qbwd.done, c->B,
+                                                                       c->epoch_bwd, c->L, c->Lsize, x, c->n,
+                                                                       c->max_m, skip);
+  DBG_SYNC("k_bwd_persist");
+  if (c->nsub > 0)
+    k_bwd_tiny<<<(c->nsub * c->B + 255) / 256, 256, 0, st>>>(c->S, c->sub_ptr, c->sub_nodes, c->nsub, c->B, c->L,
+                                                              c->Lsize, x, c->n, skip);
+  DBG_SYNC("k_bwd_tiny");
+}
+
 // x <- K^{-1} x  (internal order, in place), skipping instances with skip[b]
 void ksolve(ckkt_ctx* c, double* x, const int* skip) {
   const auto& A = c->A;
   cudaStream_t st = c->stream;
-  const size_t sms = sizeof(double) * SMALL_WARPS * (c->max_m + 32);
-  const size_t smb = sizeof(double) * (c->max_m + 64);
-  for (int l = 0; l < A.nlevels; ++l) {
-    const int ns_ = c->lsmall_ptr[l + 1] - c->lsmall_ptr[l], nb_ = c->lbig_ptr[l + 1] - c->lbig_ptr[l];
-    if (ns_ > 0)
-      k_fwd_small<<<dim3((ns_ + SMALL_WARPS - 1) / SMALL_WARPS, c->B), 32 * SMALL_WARPS, sms, st>>>(
-          c->S, c->lsmall + c->lsmall_ptr[l], ns_, c->L, c->Lsize, x, c->n, c->Vb, c->Vsize, c->max_m, skip);
-    if (nb_ > 0)
-      k_fwd_big<<<dim3(nb_, c->B), BIG_THREADS, smb, st>>>(c->S, c->lbig + c->lbig_ptr[l], c->L, c->Lsize, x, c->n,
-                                                            c->Vb, c->Vsize, skip);
-  }
-  for (int l = A.nlevels - 1; l >= 0; --l) {
-    const int ns_ = c->lsmall_ptr[l + 1] - c->lsmall_ptr[l], nb_ = c->lbig_ptr[l + 1] - c->lbig_ptr[l];
-    if (nb_ > 0)
-      k_bwd_big<<<dim3(nb_, c->B), BIG_THREADS, smb, st>>>(c->S, c->lbig + c->lbig_ptr[l], c->L, c->Lsize, x, c->n,
-                                                            skip);
-    if (ns_ > 0)
-      k_bwd_small<<<dim3((ns_ + SMALL_WARPS - 1) / SMALL_WARPS, c->B), 32 * SMALL_WARPS, sms, st>>>(
-          c->S, c->lsmall + c->lsmall_ptr[l], ns_, c->L, c->Lsize, x, c->n, c->max_m, skip);
-  }
-  int64_t nl = 0;
-  for (int l = 0; l < A.nlevels; ++l)
-    nl += (c->lsmall_ptr[l + 1] > c->lsmall_ptr[l]) + (c->lbig_ptr[l + 1] > c->lbig_ptr[l]);
-  c->launches += 2 * nl;
+  launch_fwd(c, x, skip);
+  launch_bwd(c, x, skip);
+  c->launches += 2 * ((c->nq > 0) + (c->nsub > 0));
+
 }
 
 void dot(ckkt_ctx* c, int64_t len, const double* a, const double* b, const int* skip) {
@@ -1201,6 +1289,61 @@ extern "C" ckkt_status ckkt_iterate_host(ckkt_ctx* c, const double* w_val, const
 //         5 = srows, 6 = pofs (int64), 7 = kp (int64), 8 = ki
 // Returns the element count when host == NULL.
 // ---------------------------------------------------------------------------------------------
+// Debug timing of the kernels of one triangular solve pair on x = ones (ms, averaged over reps):
+// out[0] = forward sweep, out[1] = backward sweep, out[2] = refactor.
+extern "C" int ckkt_debug_time(ckkt_ctx* c, int reps, double* out) {
+  if (!c || !c->has_device || !c->factored) return CKKT_INVALID_ARG;
+  {
+    int nw = getenv("CKKT_NOWAIT") ? 1 : 0;
+    cudaMemcpyToSymbol(g_debug_nowait, &nw, sizeof(int));
+  }
+  cudaStream_t st = c->stream;
+  const auto& A = c->A;
+  cudaEvent_t e0, e1, e2;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventCreate(&e2);
+  float f = 0, b = 0, t;
+  for (int r = 0; r < reps; ++r) {
+    cudaEventRecord(e0, st);
+    launch_fwd(c, c->tn, nullptr);
+    cudaEventRecord(e1, st);
+    launch_bwd(c, c->tn, nullptr);
+    cudaEventRecord(e2, st);
+    cudaEventSynchronize(e2);
+    cudaEventElapsedTime(&t, e0, e1);
+    f += t;
+    cudaEventElapsedTime(&t, e1, e2);
+    b += t;
+  }
+  out[0] = f / reps;
+  out[1] = b / reps;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaEventDestroy(e2);
+  return cudaGetLastError() == cudaSuccess ? 0 : CKKT_CUDA_ERROR;
+}
+
+// Debug: run one backward sweep recording per-supernode (ticket, wake, end, warp) timestamps.
+extern "C" int ckkt_debug_trace_bwd(ckkt_ctx* c, unsigned long long* host_ts) {
+  if (!c || !c->has_device || !c->factored) return CKKT_INVALID_ARG;
+  {
+    int nw = getenv("CKKT_NOWAIT") ? 1 : 0;
+    cudaMemcpyToSymbol(g_debug_nowait, &nw, sizeof(int));
+  }
+  unsigned long long* d = nullptr;
+  cudaMalloc(&d, sizeof(unsigned long long) * 4 * c->A.ns);
+  cudaMemset(d, 0, sizeof(unsigned long long) * 4 * c->A.ns);
+  cudaMemcpyToSymbol(g_debug_ts, &d, sizeof(d));
+  launch_bwd(c, c->tn, nullptr);
+  cudaStreamSynchronize(c->stream);
+  cudaMemcpy(host_ts, d, sizeof(unsigned long long) * 4 * c->A.ns, cudaMemcpyDeviceToHost);
+  unsigned long long* z = nullptr;
+  cudaMemcpyToSymbol(g_debug_ts, &z, sizeof(z));
+  cudaFree(d);
+  return 0;
+}
+
 extern "C" const char* ckkt_debug_error_string() { return cudaGetErrorString(last_cuda_error); }
 
 extern "C" int64_t ckkt_debug_get(const ckkt_ctx* c, int what, void* host) {
