@@ -40,7 +40,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ckkt", choices=["ckkt", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
-    ap.add_argument("--leaf", type=int, default=268)
+    ap.add_argument("--leaf", type=int, default=1072)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-lifted", action="store_true")
@@ -156,8 +156,8 @@ def run_ckkt(args, world, rank, local):
     if world > 1:
         torch.distributed.barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    # phase timing for the roofline (refactor = condensation + factorization)
     l0 = ctx.launch_count()
+    ctx.profile(True)  # CUDA events around every condense / factor / forward / backward launch
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         ev0.record(stream)
@@ -167,6 +167,8 @@ def run_ckkt(args, world, rank, local):
         ev1.record(stream)
         torch.cuda.synchronize()
     launches = ctx.launch_count() - l0
+    phases = ctx.phase_times()
+    ctx.profile(False)
     ms = ev0.elapsed_time(ev1)
     if world > 1:
         import torch.distributed as tdist
@@ -174,22 +176,6 @@ def run_ckkt(args, world, rank, local):
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
         tdist.barrier()
         ms = float(t.item())
-    # phase breakdown (separate short run): refactor alone and solve alone
-    evs = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-    fac_ms, sol_ms = [], []
-    for k in range(min(args.steps, 5)):
-        kk = k % T
-        torch.cuda.synchronize()
-        evs[0].record(stream)
-        ctx.refactor(data["w"][kk], data["j"][kk], None, data["sig"][kk], None, None, notpd, None)
-        evs[1].record(stream)
-        ctx.solve(data["r1"][kk], None, data["ra"][kk], None, dx, None, dy, None, want_info=False)
-        evs[2].record(stream)
-        torch.cuda.synchronize()
-        fac_ms.append(evs[0].elapsed_time(evs[1]))
-        sol_ms.append(evs[1].elapsed_time(evs[2]))
-    fac_ms = float(np.median(fac_ms))
-    sol_ms = float(np.median(sol_ms))
     # Lifted-KKT on the same instance (extra key)
     lifted = None
     if not args.no_lifted:
@@ -253,14 +239,31 @@ def run_ckkt(args, world, rank, local):
         return
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
-    # roofline of the refactorization (condensation + factorization): algorithmic bytes =
-    # read W, J, Sigma values + write/read K + write L; see DESIGN.md §7.
-    w_nnz, j_nnz = len(pat.w_row), len(pat.j_col)
-    fac_bytes = 8.0 * (w_nnz + j_nnz + n + 2 * sizes["nnz_k"] + sizes["nnz_l"])
-    achieved = fac_bytes / (fac_ms * 1e-3) / 1e9
-    roof = {"bound": "hbm", "kernel": "refactor (k_condense + k_factor levels)", "achieved": achieved,
-            "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": None,
-            "algorithmic_bytes": fac_bytes, "ms": fac_ms}
+    # roofline of the dominant kernel phase: algorithmic bytes per launch
+    #   forward / backward sweep: read every panel once + read/write x   = 8 (l_storage + 2 n)
+    #   factorization:            read K, write L                        = 8 (nnz_k + l_storage)
+    #   condensation:             read W, J, Sigma, maps; write K
+    algo = {"forward": 8.0 * (sizes["l_storage"] + 2 * n), "backward": 8.0 * (sizes["l_storage"] + 2 * n),
+            "factor": 8.0 * (sizes["nnz_k"] + sizes["l_storage"]),
+            "condense": 8.0 * (len(pat.w_row) + len(pat.j_col) + n + sizes["nnz_k"])}
+    dom = max(phases, key=lambda k: phases[k][0])
+    dom_ms, dom_n = phases[dom]
+    avg = dom_ms / max(dom_n, 1)
+    achieved = algo[dom] / (avg * 1e-3) / 1e9
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "when" in peaks else "fallback"
+    roof = {"bound": "hbm", "kernel": {"forward": "k_fwd_tiny + k_fwd_persist (one forward sweep)",
+                                       "backward": "k_bwd_persist + k_bwd_tiny (one backward sweep)",
+                                       "factor": "k_factor_persist", "condense": "k_condense"}[dom],
+            "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+            "traffic": None, "peak_source": peak_src, "algorithmic_bytes_per_launch": algo[dom],
+            "avg_launch_ms": avg,
+            "phases_ms_per_step": {k: v[0] / args.steps for k, v in phases.items()},
+            "launches_per_step": {k: v[1] / args.steps for k, v in phases.items()}}
+    fac_ms = phases["factor"][0] / max(phases["factor"][1], 1)
+    fp64 = {"kernel": "k_factor_persist", "flops": sizes["flops_factor"], "ms": fac_ms,
+            "achieved_tflops": sizes["flops_factor"] / (fac_ms * 1e-3) / 1e12, "peak_tflops": 37.1,
+            "peak_source": "measured DFMA/DMMA microbenchmark, profiles/fp64_peak_r01.txt"}
+    fp64["frac"] = fp64["achieved_tflops"] / fp64["peak_tflops"]
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         cpu = cpu_baseline(data, args)
@@ -283,13 +286,16 @@ def run_ckkt(args, world, rank, local):
         "config": {"workload": desc, "N": N, "n": n, "m_e": m, "strategy": "HyKKT gamma=1e7",
                    "leaf": args.leaf, "l2": "inputs larger than L2 (L factor %.2f GB)" % (sizes["l_storage"] * 8 / 1e9),
                    "parallelism": f"replicas x{world}"},
-        "phases_ms": {"refactor": fac_ms, "solve": sol_ms},
+        "phases_ms": {"refactor": (phases["condense"][0] + phases["factor"][0]) / args.steps,
+                      "sweeps": (phases["forward"][0] + phases["backward"][0]) / args.steps,
+                      "other": ms / args.steps - sum(v[0] for v in phases.values()) / args.steps},
         "solver": info_summary,
         "lifted": lifted,
         "sizes": sizes,
         "setup_s": setup_s,
         "gen_s": t1 - t0,
         "roofline": roof,
+        "factor_fp64": fp64,
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clk.summary(),

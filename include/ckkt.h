@@ -156,6 +156,14 @@ ckkt_status ckkt_iterate_host(ckkt_ctx *ctx, const double *w_val, const double *
                               const double *r1, const double *r2, const double *r3, const double *r4,
                               double *dx, double *ds, double *dy, double *dz, int32_t *not_pd, ckkt_info *info);
 
+/* Phase profiling (telemetry for the roofline report): when enabled, CUDA events are recorded on
+ * the context's stream around every launch of the phases
+ *   0 = condensation (k_condense), 1 = numeric factorization, 2 = forward sweeps, 3 = backward sweeps.
+ * ckkt_phase_times synchronises the stream, returns the accumulated device milliseconds and launch
+ * counts per phase since the previous call (or since enabling), and resets them. */
+ckkt_status ckkt_profile(ckkt_ctx *ctx, int32_t enable);
+ckkt_status ckkt_phase_times(ckkt_ctx *ctx, double *ms /* [4] */, int64_t *count /* [4] */);
+
 /* Number of CUDA kernel launches enqueued by this context since creation (telemetry). */
 int64_t ckkt_launch_count(const ckkt_ctx *ctx);
 

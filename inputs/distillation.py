@@ -348,8 +348,8 @@ class Model:
         x, y, u, L, V = self.split(v)
         return float(np.sum(self.p.w_x * (x[1:, 0] - self.p.xbar1) ** 2 + self.p.rho * (u[1:] - self.p.ubar) ** 2))
 
-    def hessian_values(self, v: np.ndarray, lam: np.ndarray) -> np.ndarray:
-        """W = ∇²f + Σ_r λ_r ∇²g_r in the sorted lower pattern order of build_pattern."""
+    def hessian_values(self, v: np.ndarray, lam: np.ndarray, obj_weight: float = 1.0) -> np.ndarray:
+        """W = obj_weight ∇²f + Σ_r λ_r ∇²g_r in the sorted lower pattern order of build_pattern."""
         x, y, u, L, V = self.split(v)
         p, M, N = self.p, self.M, self.N
         lam = lam.reshape(N + 1, NR)
@@ -364,8 +364,8 @@ class Model:
         if N >= 1:
             xs = x[1:]
             dxx = -lv[1:] * self.vle_d2(xs)
-            dxx[:, 0] += 2 * p.w_x
-            duu = np.full(N, 2 * p.rho)
+            dxx[:, 0] += 2 * p.w_x * obj_weight
+            duu = np.full(N, 2 * p.rho * obj_weight)
             # (L, x_k), k = 1..31 (0-based 0..30)
             dLx = np.zeros((N, NT - 1))
             for k0 in range(NT - 1):         # x_{k0+1}
@@ -415,11 +415,22 @@ class Iterate:
     d_lifted: np.ndarray # slack diagonal D of the relaxed rows (m), Lifted-KKT
 
 
+MAX_GRADIENT = 100.0  # gradient-based NLP scaling of MadNLP/Ipopt (reading R14)
+
+
 class Instance:
     """One NMPC instance (initial state seeded by 1000 + i) with its base
-    trajectory, multipliers and IPM-like iterates."""
+    trajectory, multipliers and IPM-like iterates.
 
-    def __init__(self, N: int, instance: int = 0, params: Params = Params(), lsqr_iters: int = 60):
+    scaled=True (default, reading R14): the iterates are those of the gradient-scaled NLP that an
+    Ipopt-style solver such as MadNLP factorizes by default (P:62 cites [wachter2006implementation];
+    the paper only sets tol and gamma): objective scale s_f = min(1, 100/||grad f(x0)||_inf) and
+    constraint row scales s_r = min(1, 100/||grad g_r(x0)||_inf), fixed at the base point.  J rows
+    are multiplied by s_r, the multipliers are those of the scaled problem and
+    W = s_f grad^2 f + sum_r lam_r s_r grad^2 g_r."""
+
+    def __init__(self, N: int, instance: int = 0, params: Params = Params(), lsqr_iters: int = 60,
+                 scaled: bool = True):
         self.model = Model(N, params)
         md = self.model
         p = params
@@ -435,8 +446,19 @@ class Instance:
         from scipy.sparse import csr_matrix
         from scipy.sparse.linalg import lsqr
         pat = md.pat
-        J = csr_matrix((md.jacobian_values(self.v), pat.j_col, pat.j_rowptr), shape=(md.m, md.n))
-        self.lam = lsqr(J.T.tocsr(), -md.grad_f(self.v), atol=0, btol=0, iter_lim=lsqr_iters)[0]
+        jv = md.jacobian_values(self.v)
+        self.rows_of_entries = np.repeat(np.arange(md.m), np.diff(pat.j_rowptr))
+        if scaled:
+            rowmax = np.zeros(md.m)
+            np.maximum.at(rowmax, self.rows_of_entries, np.abs(jv))
+            self.row_scale = np.minimum(1.0, MAX_GRADIENT / np.maximum(rowmax, 1e-300))
+            gmax = np.abs(md.grad_f(self.v)).max()
+            self.obj_scale = min(1.0, MAX_GRADIENT / gmax) if gmax > 0 else 1.0
+        else:
+            self.row_scale = np.ones(md.m)
+            self.obj_scale = 1.0
+        J = csr_matrix((jv * self.row_scale[self.rows_of_entries], pat.j_col, pat.j_rowptr), shape=(md.m, md.n))
+        self.lam = lsqr(J.T.tocsr(), -self.obj_scale * md.grad_f(self.v), atol=0, btol=0, iter_lim=lsqr_iters)[0]
         self.instance = instance
 
     def iterate(self, k: int, mu: float) -> Iterate:
@@ -455,8 +477,9 @@ class Instance:
         sigma[:, OU] = mu / (u - p.u_lo) ** 2 + mu / (p.u_hi - u) ** 2
         s = 0.9 * TAU * rng.uniform(-1, 1, md.m)
         d = mu / (s + TAU) ** 2 + mu / (TAU - s) ** 2
-        return Iterate(mu=mu, v=v, lam=lam, w_val=md.hessian_values(v, lam), j_val=md.jacobian_values(v),
-                       sigma_x=sigma.ravel(), d_lifted=d)
+        rs = self.row_scale
+        return Iterate(mu=mu, v=v, lam=lam, w_val=md.hessian_values(v, lam * rs, self.obj_scale),
+                       j_val=md.jacobian_values(v) * rs[self.rows_of_entries], sigma_x=sigma.ravel(), d_lifted=d)
 
     def trajectory(self, per_mu: int = 3):
         """~18 iterates: 3 per barrier value of mu_schedule()."""

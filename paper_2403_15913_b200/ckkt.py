@@ -20,7 +20,9 @@ CKKT_PATTERN_ERROR, CKKT_INVALID_ARG, CKKT_CUDA_ERROR, CKKT_OUT_OF_MEMORY = 4, 5
 CKKT_LIFTED, CKKT_HYKKT = 0, 1
 
 EXPORTED = ["ckkt_default_options", "ckkt_setup", "ckkt_get_sizes", "ckkt_export_symbolic", "ckkt_refactor",
-            "ckkt_solve", "ckkt_iterate_host", "ckkt_launch_count", "ckkt_destroy", "ckkt_status_str"]
+            "ckkt_solve", "ckkt_iterate_host", "ckkt_profile", "ckkt_phase_times", "ckkt_launch_count",
+            "ckkt_destroy", "ckkt_status_str"]
+PHASES = ("condense", "factor", "forward", "backward")
 
 
 class ckkt_pattern(ctypes.Structure):
@@ -81,6 +83,10 @@ def lib():
         L.ckkt_solve.restype = ctypes.c_int
         L.ckkt_iterate_host.argtypes = [P] * 16 + [ctypes.POINTER(ckkt_info)]
         L.ckkt_iterate_host.restype = ctypes.c_int
+        L.ckkt_profile.argtypes = [P, ctypes.c_int32]
+        L.ckkt_profile.restype = ctypes.c_int
+        L.ckkt_phase_times.argtypes = [P, P, P]
+        L.ckkt_phase_times.restype = ctypes.c_int
         L.ckkt_launch_count.argtypes = [P]
         L.ckkt_launch_count.restype = ctypes.c_int64
         L.ckkt_destroy.argtypes = [P]
@@ -198,6 +204,20 @@ class Context:
         if rc:
             raise CKKTError(rc, "ckkt_export_symbolic")
         return perm, parent, cc, Lp, Li
+
+    def profile(self, enable: bool = True):
+        rc = lib().ckkt_profile(self.h, int(enable))
+        if rc:
+            raise CKKTError(rc, "ckkt_profile")
+
+    def phase_times(self) -> dict:
+        """{phase: (ms, launches)} accumulated since the previous call (synchronises the stream)."""
+        ms = np.zeros(4)
+        cnt = np.zeros(4, np.int64)
+        rc = lib().ckkt_phase_times(self.h, _np_ptr(ms), _np_ptr(cnt))
+        if rc:
+            raise CKKTError(rc, "ckkt_phase_times")
+        return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(PHASES)}
 
     def launch_count(self) -> int:
         return int(lib().ckkt_launch_count(self.h))

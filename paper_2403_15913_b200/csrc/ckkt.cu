@@ -491,6 +491,12 @@ struct ckkt_ctx {
   int nchunk = 0, nq = 0, nsub = 0;
   int32_t *chunk_ptr = nullptr, *queue = nullptr, *sub_ptr = nullptr, *sub_nodes = nullptr;
   int8_t* tinyflag = nullptr;
+  // phase profiling
+  bool profiling = false;
+  std::vector<std::array<cudaEvent_t, 2>> ev_pool;
+  std::vector<int> ev_phase;
+  size_t ev_used = 0;
+  int prof_phase = -1;
   int64_t big_smem = 0, fac_smem = 0, sol_smem = 0;
   int *notpd = nullptr, *minpiv = nullptr;
   // last refactor values (caller-owned, must stay valid until the next refactor)
@@ -518,6 +524,24 @@ struct ckkt_ctx {
 };
 
 namespace {
+
+void prof_begin(ckkt_ctx* c, int phase) {
+  if (!c->profiling) return;
+  if (c->ev_used == c->ev_pool.size()) {
+    std::array<cudaEvent_t, 2> e;
+    cudaEventCreate(&e[0]);
+    cudaEventCreate(&e[1]);
+    c->ev_pool.push_back(e);
+    c->ev_phase.push_back(phase);
+  }
+  c->ev_phase[c->ev_used] = phase;
+  cudaEventRecord(c->ev_pool[c->ev_used][0], c->stream);
+}
+void prof_end(ckkt_ctx* c) {
+  if (!c->profiling) return;
+  cudaEventRecord(c->ev_pool[c->ev_used][1], c->stream);
+  ++c->ev_used;
+}
 
 ckkt_status dalloc(ckkt_ctx* c, void** p, size_t bytes) {
   if (bytes == 0) bytes = 8;
@@ -808,6 +832,10 @@ void ckkt_destroy(ckkt_ctx* c) {
   if (!c) return;
   if (c->has_device) {
     cudaSetDevice(c->opt.device);
+    for (auto& e : c->ev_pool) {
+      cudaEventDestroy(e[0]);
+      cudaEventDestroy(e[1]);
+    }
     for (void* p : c->owned) cudaFree(p);
     if (c->h_pinned_int) cudaFreeHost(c->h_pinned_int);
     if (c->h_pinned_dbl) cudaFreeHost(c->h_pinned_dbl);
@@ -914,6 +942,30 @@ ckkt_status ckkt_export_symbolic(const ckkt_ctx* c, int32_t* perm, int32_t* pare
 
 int64_t ckkt_launch_count(const ckkt_ctx* c) { return c ? c->launches : 0; }
 
+ckkt_status ckkt_profile(ckkt_ctx* c, int32_t enable) {
+  if (!c || !c->has_device) return CKKT_INVALID_ARG;
+  c->profiling = enable != 0;
+  c->ev_used = 0;
+  return CKKT_OK;
+}
+
+ckkt_status ckkt_phase_times(ckkt_ctx* c, double* ms, int64_t* count) {
+  if (!c || !c->has_device || !ms || !count) return CKKT_INVALID_ARG;
+  for (int k = 0; k < 4; ++k) {
+    ms[k] = 0.0;
+    count[k] = 0;
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  for (size_t i = 0; i < c->ev_used; ++i) {
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, c->ev_pool[i][0], c->ev_pool[i][1]));
+    ms[c->ev_phase[i]] += t;
+    count[c->ev_phase[i]]++;
+  }
+  c->ev_used = 0;
+  return CKKT_OK;
+}
+
 ckkt_status ckkt_refactor(ckkt_ctx* c, const double* w_val, const double* g_val, const double* h_val,
                           const double* sigma_x, const double* d_s, const double* delta_x, int32_t* not_pd,
                           int32_t* min_bad_pivot) {
@@ -931,18 +983,22 @@ ckkt_status ckkt_refactor(ckkt_ctx* c, const double* w_val, const double* g_val,
   c->delta = delta_x;
   const double gamma = (c->opt.strategy == CKKT_HYKKT) ? c->opt.gamma : 0.0;
   k_init_flags<<<nblk(B), TPB, 0, st>>>(B, c->notpd, c->minpiv);
+  prof_begin(c, 0);
   k_condense<<<dim3(nblk(c->nnzk), B), TPB, 0, st>>>(c->nnzk, c->wt_ptr, c->wt_idx, c->jt_ptr, c->jt_a, c->jt_b,
                                                      c->jt_r, c->kdiag, w_val, c->w_nnz, g_val, c->g_nnz, h_val,
                                                      c->h_nnz, sigma_x, d_s, delta_x, gamma, c->n, c->me, c->mi,
                                                      c->Kval);
   DBG_SYNC("k_condense");
+  prof_end(c);
   c->launches += 2;
   const auto& A = c->A;
   ++c->epoch_fac;
+  prof_begin(c, 1);
   k_factor_persist<<<c->grid_fac, MF_THREADS, c->fac_smem, st>>>(c->S, c->Qfac, A.ns, B, c->epoch_fac, c->L, c->Lsize,
                                                                  c->Ub, c->Usize, c->Kval, c->nnzk, c->notpd,
                                                                  c->minpiv);
   DBG_SYNC("k_factor_persist");
+  prof_end(c);
   c->launches++;
   k_final_flags<<<nblk(B), TPB, 0, st>>>(B, c->notpd, c->minpiv, c->S.perm2, not_pd, min_bad_pivot);
   c->launches++;
@@ -957,6 +1013,7 @@ namespace {
 
 void launch_fwd(ckkt_ctx* c, double* x, const int* skip) {
   cudaStream_t st = c->stream;
+  prof_begin(c, 2);
   if (c->nsub > 0)
     k_fwd_tiny<<<(c->nsub * c->B + 255) / 256, 256, 0, st>>>(c->S, c->sub_ptr, c->sub_nodes, c->nsub, c->B, c->L,
                                                               c->Lsize, x, c->n, c->Vb, c->Vsize, skip);
@@ -968,10 +1025,12 @@ void launch_fwd(ckkt_ctx* c, double* x, const int* skip) {
                                                                        c->epoch_fwd, c->L, c->Lsize, x, c->n, c->Vb,
                                                                        c->Vsize, c->max_m, skip, c->tinyflag);
   DBG_SYNC("k_fwd_persist");
+  prof_end(c);
 }
 
 void launch_bwd(ckkt_ctx* c, double* x, const int* skip) {
   cudaStream_t st = c->stream;
+  prof_begin(c, 3);
   ++c->epoch_bwd;
   if (c->nq > 0)
     k_bwd_persist<<<c->grid_bwd, 32 * SOLVE_WARPS, c->sol_smem, st>>>(c->S, c->queue, c->chunk_ptr, c->nchunk,
@@ -983,6 +1042,7 @@ void launch_bwd(ckkt_ctx* c, double* x, const int* skip) {
     k_bwd_tiny<<<(c->nsub * c->B + 255) / 256, 256, 0, st>>>(c->S, c->sub_ptr, c->sub_nodes, c->nsub, c->B, c->L,
                                                               c->Lsize, x, c->n, skip);
   DBG_SYNC("k_bwd_tiny");
+  prof_end(c);
 }
 
 // x <- K^{-1} x  (internal order, in place), skipping instances with skip[b]

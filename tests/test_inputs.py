@@ -123,3 +123,29 @@ def test_mu_schedule_formula():
     mus = dist.mu_schedule()
     assert abs(mus[1] - 0.02) < 1e-15
     assert abs(max(1e-7, min(0.2 * 0.01, 0.01 ** 1.5)) - 0.001) < 1e-15
+
+
+def test_gradient_scaling_reading_r14():
+    """Scaled iterates: every Jacobian row has max |entry| <= 100 at the base point, and the
+    scaled W equals s_f grad^2 f + sum_r (lam_r s_r) grad^2 g_r (autograd on the scaled Lagrangian)."""
+    import torch
+    inst = dist.Instance(3)
+    md = inst.model
+    it = inst.iterate(0, 0.1)
+    base = md.jacobian_values(inst.v) * inst.row_scale[inst.rows_of_entries]
+    rowmax = np.zeros(md.m)
+    np.maximum.at(rowmax, inst.rows_of_entries, np.abs(base))
+    assert rowmax.max() <= 100.0 * (1 + 1e-12)
+    g_fn, f_fn = _torch_model(md, inst.xbar0)
+    vt = torch.tensor(it.v)
+    sl = torch.tensor(it.lam * inst.row_scale)
+    Href = torch.autograd.functional.hessian(lambda z: inst.obj_scale * f_fn(z) + sl @ g_fn(z), vt).numpy()
+    pat = md.pat
+    W = np.zeros((md.n, md.n))
+    W[pat.w_row, pat.w_col] = it.w_val
+    W = W + np.tril(W, -1).T
+    assert np.abs(W - Href).max() < 1e-9 * max(1.0, np.abs(Href).max())
+    Jref = torch.autograd.functional.jacobian(g_fn, vt).numpy() * inst.row_scale[:, None]
+    J = np.zeros((md.m, md.n))
+    J[inst.rows_of_entries, pat.j_col] = it.j_val
+    assert np.abs(J - Jref).max() < 1e-10

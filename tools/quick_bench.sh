@@ -7,7 +7,7 @@ for cl in $1; do
 import json
 try:
     d=json.load(open('gpurun_out/bench_${c}_${L}.json'))
-    print('${c}:${L}', 'hykkt=%.2fms'%d['value'], 'phases', {k:round(v,2) for k,v in d['phases_ms'].items()}, 'solver', d['solver'], 'lifted', d['lifted'], 'levels', d['sizes']['n_levels'], 'ns', d['sizes']['n_supernodes'], 'launches/step', d['gpu_launches']//d['steps'], 'setup', round(d['setup_s'],1))
+    print('${c}:${L}', 'hykkt=%.2fms'%d['value'], 'phases', {k:round(v,2) for k,v in d['phases_ms'].items()}, 'roof', round(d['roofline']['frac'],4), d['roofline']['kernel'][:12], 'fp64', round(d['factor_fp64']['achieved_tflops'],3), 'solver', d['solver'], 'lifted', d['lifted'], 'levels', d['sizes']['n_levels'], 'ns', d['sizes']['n_supernodes'], 'launches/step', d['gpu_launches']//d['steps'], 'setup', round(d['setup_s'],1))
 except Exception as e:
     print('${c}:${L} FAILED', e); print(open('gpurun_out/bench_${c}_${L}.err').read()[-2000:])
 PY
