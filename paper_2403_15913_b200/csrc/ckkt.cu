@@ -489,8 +489,11 @@ struct ckkt_ctx {
   int epoch_fac = 0, epoch_fwd = 0, epoch_bwd = 0;
   Sched Qfac{}, Qfwd{}, Qbwd{};
   int nchunk = 0, nq = 0, nsub = 0;
-  int32_t *chunk_ptr = nullptr, *queue = nullptr, *sub_ptr = nullptr, *sub_nodes = nullptr;
+  int32_t *chunk_ptr = nullptr, *queue = nullptr, *sub_ptr = nullptr, *sub_nodes = nullptr, *topq = nullptr;
+  int ntop = 0;
   int8_t* tinyflag = nullptr;
+  std::vector<int8_t> tiny_host;
+  std::vector<SnMeta> meta_h;
   // phase profiling
   bool profiling = false;
   std::vector<std::array<cudaEvent_t, 2>> ev_pool;
@@ -587,15 +590,56 @@ ckkt_status setup_device(ckkt_ctx* c) {
   UP(kmap, A.kmap);
   UP(perm2, A.perm2);
   UP(sparent, A.sparent);
-  c->S = SymDev{sfirst, srowptr, srows, pofs, level_list, ch_ptr, ch_list, relofs, relmap, uofs, vofs, kp, kmap, perm2,
-                sparent};
-  {  // persistent-kernel tasks in level order: big supernodes (one CTA) and bundles of small ones (one warp each)
+  std::vector<int32_t> relw_h(A.ns, 0);
+  for (int cc = 0; cc < A.ns; ++cc) {
+    const int p = A.sparent[cc];
+    if (p < 0) continue;
+    const int wp_ = A.sfirst[p + 1] - A.sfirst[p];
+    const int mc = (int)(A.srowptr[cc + 1] - A.srowptr[cc]) - (A.sfirst[cc + 1] - A.sfirst[cc]);
+    int k = 0;
+    while (k < mc && A.relmap[A.relofs[cc] + k] < wp_) ++k;
+    relw_h[cc] = k;
+  }
+  int32_t* relw;
+  UP(relw, relw_h);
+  // packed metadata (the tiny flags of ChMeta are filled in once the tiny subtrees are known)
+  c->meta_h.resize(A.ns);
+  for (int s2 = 0; s2 < A.ns; ++s2) {
+    SnMeta& M = c->meta_h[s2];
+    M.f = A.sfirst[s2];
+    M.w = A.sfirst[s2 + 1] - A.sfirst[s2];
+    M.m = (int)(A.srowptr[s2 + 1] - A.srowptr[s2]);
+    M.ch0 = A.ch_ptr[s2];
+    M.ch1 = A.ch_ptr[s2 + 1];
+    M.relw = relw_h[s2];
+    M.pad0 = M.pad1 = 0;
+    M.pofs = A.pofs[s2];
+    M.vofs = A.vofs[s2];
+    M.relofs = A.relofs[s2];
+    M.r0 = A.srowptr[s2];
+  }
+  c->S = SymDev{nullptr, nullptr, sfirst, srowptr, srows, pofs, level_list, ch_ptr, ch_list, relofs, relmap, uofs, vofs,
+                kp, kmap, perm2, sparent, relw};
+  {  // tiny supernodes (m <= TINY_M, w <= TINY_W, all descendants tiny): one thread per tiny subtree
+    const int ns = A.ns;
+    c->tiny_host.assign(ns, 0);
+    std::vector<int8_t>& T = c->tiny_host;
+    for (int s = 0; s < ns; ++s) {  // postorder: children before parents
+      const int64_t m = A.srowptr[s + 1] - A.srowptr[s], w = A.sfirst[s + 1] - A.sfirst[s];
+      bool t = m <= TINY_M && w <= TINY_W;
+      for (int ci = A.ch_ptr[s]; t && ci < A.ch_ptr[s + 1]; ++ci) t = T[A.ch_list[ci]] != 0;
+      T[s] = t;
+    }
+  }
+  {  // factor tasks in level order (tiny supernodes excluded): big supernodes (one CTA) and bundles of
+     // small ones (one warp each)
     std::vector<int32_t> tsn, tbig;
     c->big_smem = 0;
     for (int l = 0; l < A.nlevels; ++l) {
       std::vector<int32_t> small;
       for (int k = A.level_ptr[l]; k < A.level_ptr[l + 1]; ++k) {
         const int s = A.level_list[k];
+        if (c->tiny_host[s]) continue;
         const int64_t m = A.srowptr[s + 1] - A.srowptr[s], w = A.sfirst[s + 1] - A.sfirst[s];
         if (m * w <= SMALL_PANEL && w <= 32) {
           small.push_back(s);
@@ -616,7 +660,7 @@ ckkt_status setup_device(ckkt_ctx* c) {
     int32_t *d_tsn, *d_tbig;
     UP(d_tsn, tsn);
     UP(d_tbig, tbig);
-    std::vector<int32_t> zeros((size_t)B * A.ns, 0), z2(2, 0);
+    std::vector<int32_t> zeros((size_t)B * A.ns, 0), z2(4, 0);
     int32_t *dfac, *dfwd, *dbwd, *cfac, *cfwd, *cbwd;
     UP(dfac, zeros);
     UP(dfwd, zeros);
@@ -628,7 +672,7 @@ ckkt_status setup_device(ckkt_ctx* c) {
     c->Qfwd = Sched{c->ntask, d_tsn, d_tbig, dfwd, cfwd};
     c->Qbwd = Sched{c->ntask, d_tsn, d_tbig, dbwd, cbwd};
     c->fac_smem = std::max<int64_t>(c->big_smem, 8 * SMALL_WARPS * SMALL_PANEL);
-    c->sol_smem = 8 * SOLVE_WARPS * (c->max_m + 64 + 32 * 33);
+    c->sol_smem = 8 * ((int64_t)SOLVE_WARPS * (c->max_m + 64 + 16 * 33) + c->max_m + 128);
     if (c->fac_smem > 227 * 1024 || c->sol_smem > 227 * 1024) return CKKT_INVALID_ARG;
     CK(cudaFuncSetAttribute(k_factor_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->fac_smem));
     CK(cudaFuncSetAttribute(k_fwd_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->sol_smem));
@@ -643,13 +687,7 @@ ckkt_status setup_device(ckkt_ctx* c) {
     c->grid_bwd = std::max(1, std::min(occ * dev_sms, (A.ns * B + SOLVE_WARPS - 1) / SOLVE_WARPS));
     {  // tiny subtrees (one thread each) and the queue of the remaining supernodes (one warp each)
       const int ns = A.ns;
-      std::vector<int8_t> T(ns, 0);
-      for (int s = 0; s < ns; ++s) {  // postorder: children before parents
-        const int64_t m = A.srowptr[s + 1] - A.srowptr[s], w = A.sfirst[s + 1] - A.sfirst[s];
-        bool t = m <= TINY_M && w <= TINY_W;
-        for (int ci = A.ch_ptr[s]; t && ci < A.ch_ptr[s + 1]; ++ci) t = T[A.ch_list[ci]] != 0;
-        T[s] = t;
-      }
+      const std::vector<int8_t>& T = c->tiny_host;
       std::vector<std::vector<int32_t>> subs;
       std::vector<int32_t> stack;
       for (int s = 0; s < ns; ++s) {
@@ -675,18 +713,49 @@ ckkt_status setup_device(ckkt_ctx* c) {
         sn.insert(sn.end(), v.begin(), v.end());
         sp.push_back((int32_t)sn.size());
       }
+      {
+        std::vector<ChMeta> chm(A.ch_list.size());
+        for (size_t k = 0; k < A.ch_list.size(); ++k) {
+          const int cc = A.ch_list[k];
+          chm[k].c = cc;
+          chm[k].mc = (int)(A.srowptr[cc + 1] - A.srowptr[cc]) - (A.sfirst[cc + 1] - A.sfirst[cc]);
+          chm[k].tiny = T[cc];
+          chm[k].pad = 0;
+          chm[k].vofs = A.vofs[cc];
+          chm[k].relofs = A.relofs[cc];
+        }
+        const ChMeta* dchm = upload(chm, o, by);
+        const SnMeta* dmeta = upload(c->meta_h, o, by);
+        if (!dchm || !dmeta) return CKKT_OUT_OF_MEMORY;
+        c->S.meta = dmeta;
+        c->S.chmeta = dchm;
+      }
       c->nsub = (int)subs.size();
       c->sub_ptr = upload(sp, o, by);
       c->sub_nodes = upload(sn, o, by);
       c->tinyflag = upload(T, o, by);
-      std::vector<int32_t> q, lp{0};
+      // top set: large supernodes (panel > TOP_PANEL doubles) and all their ancestors (one CTA each)
+      std::vector<int8_t> top(ns, 0);
+      for (int s2 = 0; s2 < ns; ++s2) {
+        const int64_t m = A.srowptr[s2 + 1] - A.srowptr[s2], w = A.sfirst[s2 + 1] - A.sfirst[s2];
+        if (!T[s2] && m * w > TOP_PANEL) top[s2] = 1;
+      }
+      for (int s2 = 0; s2 < ns; ++s2)  // postorder: parents after children
+        if (top[s2] && A.sparent[s2] >= 0) top[A.sparent[s2]] = 1;
+      std::vector<int32_t> q, lp{0}, tq;
       for (int l = 0; l < A.nlevels; ++l) {
-        for (int k = A.level_ptr[l]; k < A.level_ptr[l + 1]; ++k)
-          if (!T[A.level_list[k]]) q.push_back(A.level_list[k]);
+        for (int k = A.level_ptr[l]; k < A.level_ptr[l + 1]; ++k) {
+          const int s2 = A.level_list[k];
+          if (T[s2]) continue;
+          if (top[s2]) tq.push_back(s2);
+          else q.push_back(s2);
+        }
         lp.push_back((int32_t)q.size());
       }
       c->nq = (int)q.size();
+      c->ntop = (int)tq.size();
       c->queue = upload(q, o, by);
+      c->topq = upload(tq, o, by);
       const int64_t warps = (int64_t)c->grid_fwd * SOLVE_WARPS;
       std::vector<int32_t> cp{0};
       for (int l = 0; l < A.nlevels; ++l) {
@@ -740,7 +809,7 @@ ckkt_status setup_device(ckkt_ctx* c) {
   }
 #undef UP
   DALLOC(c->Kval, (size_t)B * c->nnzk);
-  DALLOC(c->L, (size_t)B * c->Lsize);
+  DALLOC(c->L, (size_t)B * c->Lsize + 4);  // +32 B: 16-byte-rounded L2 prefetches stay in bounds
   DALLOC(c->Ub, (size_t)B * c->Usize);
   DALLOC(c->Vb, (size_t)B * c->Vsize);
   DALLOC(c->notpd, B);
@@ -994,9 +1063,15 @@ ckkt_status ckkt_refactor(ckkt_ctx* c, const double* w_val, const double* g_val,
   const auto& A = c->A;
   ++c->epoch_fac;
   prof_begin(c, 1);
-  k_factor_persist<<<c->grid_fac, MF_THREADS, c->fac_smem, st>>>(c->S, c->Qfac, A.ns, B, c->epoch_fac, c->L, c->Lsize,
-                                                                 c->Ub, c->Usize, c->Kval, c->nnzk, c->notpd,
-                                                                 c->minpiv);
+  if (c->nsub > 0)
+    k_factor_tiny<<<(c->nsub * B + 127) / 128, 128, 0, st>>>(c->S, c->sub_ptr, c->sub_nodes, c->nsub, B, c->L,
+                                                              c->Lsize, c->Ub, c->Usize, c->Kval, c->nnzk, c->notpd,
+                                                              c->minpiv);
+  DBG_SYNC("k_factor_tiny");
+  if (c->ntask > 0)
+    k_factor_persist<<<c->grid_fac, MF_THREADS, c->fac_smem, st>>>(c->S, c->Qfac, A.ns, B, c->epoch_fac, c->L,
+                                                                   c->Lsize, c->Ub, c->Usize, c->Kval, c->nnzk,
+                                                                   c->notpd, c->minpiv, c->tinyflag);
   DBG_SYNC("k_factor_persist");
   prof_end(c);
   c->launches++;
@@ -1011,6 +1086,29 @@ ckkt_status ckkt_refactor(ckkt_ctx* c, const double* w_val, const double* g_val,
 
 namespace {
 
+SweepArgs sweep_args(ckkt_ctx* c, const Sched& Q, int epoch, double* x, const int* skip) {
+  SweepArgs a;
+  a.queue = c->queue;
+  a.chunk_ptr = c->chunk_ptr;
+  a.nchunk = c->nchunk;
+  a.top = c->topq;
+  a.ntop = c->ntop;
+  a.ns = c->A.ns;
+  a.ctr = Q.ctr;
+  a.done_all = Q.done;
+  a.B = c->B;
+  a.epoch = epoch;
+  a.L = c->L;
+  a.Lsize = c->Lsize;
+  a.X = x;
+  a.n = c->n;
+  a.Vb = c->Vb;
+  a.Vsize = c->Vsize;
+  a.max_m = c->max_m;
+  a.skip = skip;
+  return a;
+}
+
 void launch_fwd(ckkt_ctx* c, double* x, const int* skip) {
   cudaStream_t st = c->stream;
   prof_begin(c, 2);
@@ -1019,11 +1117,8 @@ void launch_fwd(ckkt_ctx* c, double* x, const int* skip) {
                                                               c->Lsize, x, c->n, c->Vb, c->Vsize, skip);
   DBG_SYNC("k_fwd_tiny");
   ++c->epoch_fwd;
-  if (c->nq > 0)
-    k_fwd_persist<<<c->grid_fwd, 32 * SOLVE_WARPS, c->sol_smem, st>>>(c->S, c->queue, c->chunk_ptr, c->nchunk,
-                                                                       c->A.ns, c->Qfwd.ctr, c->Qfwd.done, c->B,
-                                                                       c->epoch_fwd, c->L, c->Lsize, x, c->n, c->Vb,
-                                                                       c->Vsize, c->max_m, skip, c->tinyflag);
+  if (c->nq + c->ntop > 0)
+    k_fwd_persist<<<c->grid_fwd, 32 * SOLVE_WARPS, c->sol_smem, st>>>(c->S, sweep_args(c, c->Qfwd, c->epoch_fwd, x, skip));
   DBG_SYNC("k_fwd_persist");
   prof_end(c);
 }
@@ -1032,11 +1127,8 @@ void launch_bwd(ckkt_ctx* c, double* x, const int* skip) {
   cudaStream_t st = c->stream;
   prof_begin(c, 3);
   ++c->epoch_bwd;
-  if (c->nq > 0)
-    k_bwd_persist<<<c->grid_bwd, 32 * SOLVE_WARPS, c->sol_smem, st>>>(c->S, c->queue, c->chunk_ptr, c->nchunk,
-                                                                       c->A.ns, c->Qbwd.ctr, c->Qbwd.done, c->B,
-                                                                       c->epoch_bwd, c->L, c->Lsize, x, c->n,
-                                                                       c->max_m, skip);
+  if (c->nq + c->ntop > 0)
+    k_bwd_persist<<<c->grid_bwd, 32 * SOLVE_WARPS, c->sol_smem, st>>>(c->S, sweep_args(c, c->Qbwd, c->epoch_bwd, x, skip));
   DBG_SYNC("k_bwd_persist");
   if (c->nsub > 0)
     k_bwd_tiny<<<(c->nsub * c->B + 255) / 256, 256, 0, st>>>(c->S, c->sub_ptr, c->sub_nodes, c->nsub, c->B, c->L,
@@ -1395,9 +1487,27 @@ extern "C" int ckkt_debug_trace_bwd(ckkt_ctx* c, unsigned long long* host_ts) {
   cudaMalloc(&d, sizeof(unsigned long long) * 4 * c->A.ns);
   cudaMemset(d, 0, sizeof(unsigned long long) * 4 * c->A.ns);
   cudaMemcpyToSymbol(g_debug_ts, &d, sizeof(d));
-  launch_bwd(c, c->tn, nullptr);
+  unsigned long long* dph = nullptr;
+  if (getenv("CKKT_TRACE_FACTOR")) {
+    cudaMalloc(&dph, sizeof(unsigned long long) * 8 * c->A.ns);
+    cudaMemset(dph, 0, sizeof(unsigned long long) * 8 * c->A.ns);
+    cudaMemcpyToSymbol(g_debug_ph, &dph, sizeof(dph));
+    ckkt_refactor(c, c->w_val, c->g_val, c->h_val, c->sigma, c->d_s, c->delta, nullptr, nullptr);
+  } else {
+    launch_bwd(c, c->tn, nullptr);
+  }
   cudaStreamSynchronize(c->stream);
   cudaMemcpy(host_ts, d, sizeof(unsigned long long) * 4 * c->A.ns, cudaMemcpyDeviceToHost);
+  if (dph) {
+    FILE* fp = fopen("/tmp/ckkt_phases.bin", "wb");
+    std::vector<unsigned long long> hph(8 * (size_t)c->A.ns);
+    cudaMemcpy(hph.data(), dph, sizeof(unsigned long long) * hph.size(), cudaMemcpyDeviceToHost);
+    fwrite(hph.data(), 8, hph.size(), fp);
+    fclose(fp);
+    unsigned long long* z2 = nullptr;
+    cudaMemcpyToSymbol(g_debug_ph, &z2, sizeof(z2));
+    cudaFree(dph);
+  }
   unsigned long long* z = nullptr;
   cudaMemcpyToSymbol(g_debug_ts, &z, sizeof(z));
   cudaFree(d);

@@ -23,7 +23,21 @@ constexpr int SMALL_PANEL = 512;   // doubles of a small supernode panel (m * w)
 constexpr int SMALL_WARPS = 8;     // warps per CTA; small supernodes per task
 constexpr int MF_THREADS = 32 * SMALL_WARPS;
 
+// packed per-supernode metadata (one 48-byte uniform load instead of several dependent loads)
+struct __align__(16) SnMeta {
+  int f, w, m, ch0;
+  int ch1, relw, pad0, pad1;
+  long long pofs, vofs, relofs, r0;
+};
+// packed per-child record, in the order of ch_list
+struct __align__(16) ChMeta {
+  int c, mc, tiny, pad;
+  long long vofs, relofs;
+};
+
 struct SymDev {
+  const SnMeta* meta;
+  const ChMeta* chmeta;
   const int32_t* sfirst;
   const int64_t* srowptr;
   const int32_t* srows;
@@ -39,6 +53,7 @@ struct SymDev {
   const int32_t* kmap;
   const int32_t* perm2;
   const int32_t* sparent;
+  const int32_t* relw;  // per child: number of its off-diagonal rows inside the parent's columns
 };
 
 struct Sched {
@@ -59,6 +74,7 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 }
 __device__ int g_debug_nowait = 0;  // debug only: skip dependency waits (timing experiments)
 __device__ unsigned long long* g_debug_ts = nullptr;  // debug only: [ns][4] ticket/wake/end times of sweeps
+__device__ unsigned long long* g_debug_ph = nullptr;  // debug only: [ns][8] phase times inside factor_big
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -93,6 +109,17 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
                : "d"(a), "d"(b));
 }
 
+// TMA bulk prefetch of [p, p + bytes) into L2 (fire and forget; 16-byte granularity)
+__device__ __forceinline__ void prefetch_l2(const void* p, int64_t bytes) {
+  uintptr_t a = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
+  const uintptr_t e = (reinterpret_cast<uintptr_t>(p) + bytes + 15) & ~uintptr_t(15);
+  while (a < e) {
+    const uint32_t sz = (uint32_t)((e - a) > (1u << 20) ? (1u << 20) : (e - a));
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(sz) : "memory");
+    a += sz;
+  }
+}
+
 __device__ __forceinline__ int off_rows(const SymDev& S, int c) {
   return (int)(S.srowptr[c + 1] - S.srowptr[c]) - (S.sfirst[c + 1] - S.sfirst[c]);
 }
@@ -108,80 +135,133 @@ __device__ __forceinline__ int next_ticket(int* ctr_slot, int* sh) {
 // ============================================================================================
 // factor
 // ============================================================================================
+// Extend-add of child c's update matrix U_c (mc x mc, lower, column-major) into the parent front:
+//   part 0: columns j < relw (targets in the parent's panel, shared memory Ps with leading dim ldp)
+//   part 1: columns j >= relw (targets in the parent's update block U, global, leading dim mu)
+// Flat iteration over U_c's column-major elements with 8 independent source (and target) loads per
+// thread per batch; targets of one child are distinct, so there are no races within a child.
+template <int PART>
+__device__ __forceinline__ void extend_add(const double* __restrict__ Uc, int mc, int relw,
+                                           const int32_t* __restrict__ rel, int w, double* Ps, int ldp, double* U,
+                                           int mu, int tid, int nt) {
+  const int e_lo = PART == 0 ? 0 : relw * mc;
+  const int e_hi = PART == 0 ? relw * mc : mc * mc;
+  for (int e0 = e_lo; e0 < e_hi; e0 += 8 * nt) {
+    double sv[8], tv[8];
+    int tgt[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int e = e0 + r * nt + tid;
+      const int j = e / mc, i = e - j * mc;
+      const bool ok = e < e_hi && i >= j;
+      sv[r] = ok ? __ldcg(Uc + e) : 0.0;
+      if (ok) {
+        const int ri = __ldg(rel + i), rj = __ldg(rel + j);
+        tgt[r] = PART == 0 ? ri + rj * ldp : (ri - w) + (rj - w) * mu;
+      } else {
+        tgt[r] = -1;
+      }
+      if (PART == 1) tv[r] = (tgt[r] >= 0) ? U[tgt[r]] : 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      if (tgt[r] < 0) continue;
+      if (PART == 0) Ps[tgt[r]] += sv[r];
+      else U[tgt[r]] = tv[r] + sv[r];
+    }
+  }
+}
+
+// Dense part of a front on the panel in shared memory (ld = ldp), by ONE warp for the w x w block
+// (w <= 64, lanes own rows lane and lane + 32), then all threads of the group for the rows below:
+//   L11 = chol(A11) (column by column, warp-synchronous), Z = L11^{-1} (row by row), L21 = A21 Z^T.
+// Returns with Ps holding [Z; L21].  GROUP_SYNC() synchronises the whole group.
+#define DENSE_FRONT(GROUP_SYNC)                                                                         \
+  if (tid < 32) {                                                                                     \
+    const int lane_ = tid;                                                                            \
+    for (int j = 0; j < w; ++j) {                                                                     \
+      double d = Ps[j + j * ldp];                                                                     \
+      if (!(d > 0.0) || !isfinite(d)) {                                                               \
+        if (lane_ == 0) {                                                                             \
+          notpd[b] = 1;                                                                               \
+          atomicMin(&minpiv[b], f + j);                                                               \
+        }                                                                                             \
+        d = nan("");                                                                                  \
+      }                                                                                               \
+      const double piv = sqrt(d);                                                                     \
+      __syncwarp();                                                                                   \
+      for (int i = j + 1 + lane_; i < w; i += 32) Ps[i + j * ldp] /= piv;                             \
+      if (lane_ == 0) Ps[j + j * ldp] = piv;                                                          \
+      __syncwarp();                                                                                   \
+      for (int i = j + 1 + lane_; i < w; i += 32) {                                                   \
+        const double lij = Ps[i + j * ldp];                                                           \
+        for (int c2 = j + 1; c2 <= i; ++c2) Ps[i + c2 * ldp] -= lij * Ps[c2 + j * ldp];               \
+      }                                                                                               \
+      __syncwarp();                                                                                   \
+    }                                                                                                 \
+    for (int i = 0; i < w; ++i) { /* Z = L11^{-1}: row i from rows < i */                             \
+      double z0 = 0.0, z1 = 0.0;                                                                      \
+      const double lii = Ps[i + i * ldp];                                                             \
+      if (lane_ <= i) {                                                                               \
+        z0 = (lane_ == i) ? 1.0 : 0.0;                                                                \
+        for (int k = lane_; k < i; ++k) z0 -= Ps[i + k * ldp] * Ps[k + lane_ * ldp];                  \
+        z0 /= lii;                                                                                    \
+      }                                                                                               \
+      if (lane_ + 32 <= i) {                                                                          \
+        z1 = (lane_ + 32 == i) ? 1.0 : 0.0;                                                           \
+        for (int k = lane_ + 32; k < i; ++k) z1 -= Ps[i + k * ldp] * Ps[k + (lane_ + 32) * ldp];      \
+        z1 /= lii;                                                                                    \
+      }                                                                                               \
+      __syncwarp();                                                                                   \
+      if (lane_ <= i) Ps[i + lane_ * ldp] = z0;                                                       \
+      if (lane_ + 32 <= i) Ps[i + (lane_ + 32) * ldp] = z1;                                           \
+      __syncwarp();                                                                                   \
+    }                                                                                                 \
+  }                                                                                                   \
+  GROUP_SYNC();                                                                                       \
+  for (int i = w + tid; i < m; i += nt) { /* L21 row i = A21 row i * Z^T (row-parallel, no barriers) */ \
+    double arow[64];                                                                                  \
+    for (int k = 0; k < w; ++k) arow[k] = Ps[i + k * ldp];                                            \
+    for (int k = 0; k < w; ++k) {                                                                     \
+      double acc = 0.0;                                                                               \
+      for (int j = 0; j <= k; ++j) acc += arow[j] * Ps[k + j * ldp];                                  \
+      Ps[i + k * ldp] = acc;                                                                          \
+    }                                                                                                 \
+  }                                                                                                   \
+  GROUP_SYNC();
+
 // small supernode, one warp, panel in shared memory (ld = m)
-__device__ void factor_small(const SymDev& S, int s, int b, int lane, double* Ps, double* L, int64_t Lsize,
+__device__ void factor_small(const SymDev& S, int s, int b, int tid, double* Ps, double* L, int64_t Lsize,
                              double* Ub, int64_t Usize, const double* __restrict__ Kb, int* notpd, int* minpiv) {
+  const int nt = 32;
   const int f = S.sfirst[s], w = S.sfirst[s + 1] - f;
   const int m = (int)(S.srowptr[s + 1] - S.srowptr[s]);
-  const int mu = m - w;
+  const int mu = m - w, ldp = m;
   double* P = L + b * Lsize + S.pofs[s];
   double* U = Ub + b * Usize + S.uofs[s];
-  for (int i = lane; i < m * w; i += 32) Ps[i] = 0.0;
+  for (int i = tid; i < m * w; i += nt) Ps[i] = 0.0;
   __syncwarp();
-  for (int64_t k = S.kp[f] + lane; k < S.kp[f + w]; k += 32) Ps[S.kmap[k]] = Kb[k];
+  for (int64_t k = S.kp[f] + tid; k < S.kp[f + w]; k += nt) Ps[S.kmap[k]] = Kb[k];
   __syncwarp();
-  for (int ci = S.ch_ptr[s]; ci < S.ch_ptr[s + 1]; ++ci) {  // panel part of the children
+  for (int ci = S.ch_ptr[s]; ci < S.ch_ptr[s + 1]; ++ci) {
     const int c = S.ch_list[ci];
-    const int mc = off_rows(S, c);
-    const double* Uc = Ub + b * Usize + S.uofs[c];
-    const int32_t* rel = S.relmap + S.relofs[c];
-    for (int j = 0; j < mc; ++j) {
-      const int rj = rel[j];
-      if (rj >= w) break;  // rel is increasing
-      for (int i = j + lane; i < mc; i += 32) Ps[rel[i] + rj * m] += __ldcg(Uc + i + (int64_t)j * mc);
-    }
+    extend_add<0>(Ub + b * Usize + S.uofs[c], off_rows(S, c), S.relw[c], S.relmap + S.relofs[c], w, Ps, ldp, U,
+                  mu, tid, nt);
     __syncwarp();
   }
-  for (int j = 0; j < w; ++j) {
-    double d = Ps[j + j * m];
-    if (!(d > 0.0) || !isfinite(d)) {
-      if (lane == 0) {
-        notpd[b] = 1;
-        atomicMin(&minpiv[b], f + j);
-      }
-      d = nan("");
-    }
-    const double piv = sqrt(d);
-    __syncwarp();
-    if (lane == 0) Ps[j + j * m] = piv;
-    for (int i = j + 1 + lane; i < m; i += 32) Ps[i + j * m] /= piv;
-    __syncwarp();
-    for (int c = j + 1; c < w; ++c) {
-      const double lc = Ps[c + j * m];
-      for (int i = c + lane; i < m; i += 32) Ps[i + c * m] -= Ps[i + j * m] * lc;
-    }
-    __syncwarp();
-  }
-  for (int i = 0; i < w; ++i) {  // L11 <- L11^{-1} (w <= 32)
-    double z = 0.0;
-    if (lane <= i) {
-      z = (lane == i) ? 1.0 : 0.0;
-      for (int k = lane; k < i; ++k) z -= Ps[i + k * m] * Ps[k + lane * m];
-      z /= Ps[i + i * m];
-    }
-    __syncwarp();
-    if (lane <= i) Ps[i + lane * m] = z;
-    __syncwarp();
-  }
-  for (int i = lane; i < m * w; i += 32) P[i] = Ps[i];
+  DENSE_FRONT(__syncwarp)
+  for (int i = tid; i < m * w; i += nt) P[i] = Ps[i];
   for (int j = 0; j < mu; ++j)  // U_s = -L21 L21^T (lower)
-    for (int i = j + lane; i < mu; i += 32) {
+    for (int i = j + tid; i < mu; i += nt) {
       double t = 0.0;
-      for (int k = 0; k < w; ++k) t += Ps[w + i + k * m] * Ps[w + j + k * m];
+      for (int k = 0; k < w; ++k) t += Ps[w + i + k * ldp] * Ps[w + j + k * ldp];
       U[i + (int64_t)j * mu] = -t;
     }
   __syncwarp();
-  for (int ci = S.ch_ptr[s]; ci < S.ch_ptr[s + 1]; ++ci) {  // trailing part of the children
+  for (int ci = S.ch_ptr[s]; ci < S.ch_ptr[s + 1]; ++ci) {
     const int c = S.ch_list[ci];
-    const int mc = off_rows(S, c);
-    const double* Uc = Ub + b * Usize + S.uofs[c];
-    const int32_t* rel = S.relmap + S.relofs[c];
-    for (int j = 0; j < mc; ++j) {
-      const int rj = rel[j];
-      if (rj < w) continue;
-      for (int i = j + lane; i < mc; i += 32)
-        U[(rel[i] - w) + (int64_t)(rj - w) * mu] += __ldcg(Uc + i + (int64_t)j * mc);
-    }
+    extend_add<1>(Ub + b * Usize + S.uofs[c], off_rows(S, c), S.relw[c], S.relmap + S.relofs[c], w, Ps, ldp, U,
+                  mu, tid, nt);
     __syncwarp();
   }
 }
@@ -194,9 +274,12 @@ __device__ void factor_big(const SymDev& S, int s, int b, double* Ps, double* pi
   const int f = S.sfirst[s], w = S.sfirst[s + 1] - f;
   const int m = (int)(S.srowptr[s + 1] - S.srowptr[s]);
   const int mu = m - w;
-  const int mp = (m + 7) & ~7, wp = (w + 3) & ~3;
+  const int mp = (m + 7) & ~7, wp = (w + 3) & ~3, ldp = mp;
   double* P = L + b * Lsize + S.pofs[s];
   double* U = Ub + b * Usize + S.uofs[s];
+  (void)piv_s;
+  unsigned long long* ph = (g_debug_ph && b == 0 && tid == 0) ? g_debug_ph + 8 * (int64_t)s : nullptr;
+  if (ph) ph[0] = gtimer();
   for (int i = tid; i < mp * wp + 8; i += nt) Ps[i] = 0.0;
   __syncthreads();
   for (int64_t k = S.kp[f] + tid; k < S.kp[f + w]; k += nt) {
@@ -204,42 +287,17 @@ __device__ void factor_big(const SymDev& S, int s, int b, double* Ps, double* pi
     Ps[(q % m) + (q / m) * mp] = Kb[k];
   }
   __syncthreads();
+  if (ph) ph[1] = gtimer();
   for (int ci = S.ch_ptr[s]; ci < S.ch_ptr[s + 1]; ++ci) {
     const int c = S.ch_list[ci];
-    const int mc = off_rows(S, c);
-    const double* Uc = Ub + b * Usize + S.uofs[c];
-    const int32_t* rel = S.relmap + S.relofs[c];
-    int jw = 0;
-    while (jw < mc && rel[jw] < w) ++jw;
-    for (int j = warp; j < jw; j += nwarp) {
-      const int rj = rel[j];
-      for (int i = j + lane; i < mc; i += 32) Ps[rel[i] + rj * mp] += __ldcg(Uc + i + (int64_t)j * mc);
-    }
+    extend_add<0>(Ub + b * Usize + S.uofs[c], off_rows(S, c), S.relw[c], S.relmap + S.relofs[c], w, Ps, ldp, U,
+                  mu, tid, nt);
     __syncthreads();
   }
-  for (int j = 0; j < w; ++j) {
-    if (tid == 0) {
-      double d = Ps[j + j * mp];
-      if (!(d > 0.0) || !isfinite(d)) {
-        notpd[b] = 1;
-        atomicMin(&minpiv[b], f + j);
-        d = nan("");
-      }
-      *piv_s = sqrt(d);
-      Ps[j + j * mp] = *piv_s;
-    }
-    __syncthreads();
-    const double pv = *piv_s;
-    for (int i = j + 1 + tid; i < m; i += nt) Ps[i + j * mp] /= pv;
-    __syncthreads();
-    const int nrest = w - j - 1;
-    for (int e = tid; e < nrest * m; e += nt) {
-      const int c = j + 1 + e / m, i = e % m;
-      if (i >= c) Ps[i + c * mp] -= Ps[i + j * mp] * Ps[c + j * mp];
-    }
-    __syncthreads();
-  }
-  {  // U_s = -L21 L21^T: 8x8 DMMA tiles of the lower triangle
+  if (ph) ph[2] = gtimer();
+  DENSE_FRONT(__syncthreads)
+  if (ph) ph[3] = gtimer();
+  {  // U_s = -L21 L21^T: 8x8 DMMA tiles of the lower triangle (Z's upper part is zero, pads are zero)
     const int nb = (mu + 7) >> 3;
     const int ntile = nb * (nb + 1) / 2;
     const int g = lane >> 2, t4 = lane & 3;
@@ -259,39 +317,23 @@ __device__ void factor_big(const SymDev& S, int s, int b, double* Ps, double* pi
       }
     }
   }
-  for (int i = 0; i < w; ++i) {  // L11 <- L11^{-1}
-    double z = 0.0;
-    const int j = tid;
-    if (j <= i) {
-      z = (j == i) ? 1.0 : 0.0;
-      for (int k = j; k < i; ++k) z -= Ps[i + k * mp] * Ps[k + j * mp];
-      z /= Ps[i + i * mp];
-    }
-    __syncthreads();
-    if (j <= i) Ps[i + j * mp] = z;
-    __syncthreads();
-  }
+  if (ph) ph[4] = gtimer();
   for (int e = tid; e < m * w; e += nt) P[e] = Ps[(e % m) + (e / m) * mp];
   __syncthreads();  // this CTA's U_s tile writes are complete before the children add into it
+  if (ph) ph[5] = gtimer();
   for (int ci = S.ch_ptr[s]; ci < S.ch_ptr[s + 1]; ++ci) {
     const int c = S.ch_list[ci];
-    const int mc = off_rows(S, c);
-    const double* Uc = Ub + b * Usize + S.uofs[c];
-    const int32_t* rel = S.relmap + S.relofs[c];
-    int jw = 0;
-    while (jw < mc && rel[jw] < w) ++jw;
-    for (int j = jw + warp; j < mc; j += nwarp) {
-      const int rj = rel[j] - w;
-      for (int i = j + lane; i < mc; i += 32)
-        U[(rel[i] - w) + (int64_t)rj * mu] += __ldcg(Uc + i + (int64_t)j * mc);
-    }
+    extend_add<1>(Ub + b * Usize + S.uofs[c], off_rows(S, c), S.relw[c], S.relmap + S.relofs[c], w, Ps, ldp, U,
+                  mu, tid, nt);
     __syncthreads();
   }
+  if (ph) ph[6] = gtimer();
 }
 
 __global__ void __launch_bounds__(MF_THREADS)
     k_factor_persist(SymDev S, Sched Q, int ns, int B, int epoch, double* L, int64_t Lsize, double* Ub,
-                     int64_t Usize, const double* __restrict__ Kval, int64_t nnzk, int* notpd, int* minpiv) {
+                     int64_t Usize, const double* __restrict__ Kval, int64_t nnzk, int* notpd, int* minpiv,
+                     const int8_t* __restrict__ tiny) {
   extern __shared__ double smem[];  // max(big panel, SMALL_WARPS small panels)
   __shared__ double piv_s;
   __shared__ int tk;
@@ -306,22 +348,40 @@ __global__ void __launch_bounds__(MF_THREADS)
     const double* Kb = Kval + b * nnzk;
     if (Q.task_big[task]) {
       const int s = Q.task_sn[task * SMALL_WARPS];
+      const unsigned long long t0 = gtimer();
       if (threadIdx.x == 0)
-        for (int ci = S.ch_ptr[s]; ci < S.ch_ptr[s + 1]; ++ci) wait_epoch(done + S.ch_list[ci], epoch);
+        for (int ci = S.ch_ptr[s]; ci < S.ch_ptr[s + 1]; ++ci)
+          if (!tiny[S.ch_list[ci]]) wait_epoch(done + S.ch_list[ci], epoch);
       __syncthreads();
+      const unsigned long long t1 = gtimer();
       factor_big(S, s, b, smem, &piv_s, L, Lsize, Ub, Usize, Kb, notpd, minpiv);
       fence_acq_rel();
       __syncthreads();
+      if (g_debug_ts && threadIdx.x == 0 && b == 0) {
+        g_debug_ts[4 * s] = t0;
+        g_debug_ts[4 * s + 1] = t1;
+        g_debug_ts[4 * s + 2] = gtimer();
+        g_debug_ts[4 * s + 3] = 1000000 + blockIdx.x;
+      }
       if (threadIdx.x == 0) st_release(done + s, epoch);
     } else {
       const int s = Q.task_sn[task * SMALL_WARPS + warp];
       if (s >= 0) {
+        const unsigned long long t0 = gtimer();
         if (lane == 0)
-          for (int ci = S.ch_ptr[s]; ci < S.ch_ptr[s + 1]; ++ci) wait_epoch(done + S.ch_list[ci], epoch);
+          for (int ci = S.ch_ptr[s]; ci < S.ch_ptr[s + 1]; ++ci)
+            if (!tiny[S.ch_list[ci]]) wait_epoch(done + S.ch_list[ci], epoch);
         __syncwarp();
+        const unsigned long long t1 = gtimer();
         factor_small(S, s, b, lane, smem + warp * SMALL_PANEL, L, Lsize, Ub, Usize, Kb, notpd, minpiv);
         fence_acq_rel();
         __syncwarp();
+        if (g_debug_ts && lane == 0 && b == 0) {
+          g_debug_ts[4 * s] = t0;
+          g_debug_ts[4 * s + 1] = t1;
+          g_debug_ts[4 * s + 2] = gtimer();
+          g_debug_ts[4 * s + 3] = blockIdx.x * 8 + warp;
+        }
         if (lane == 0) st_release(done + s, epoch);
       }
     }
@@ -334,14 +394,15 @@ __global__ void __launch_bounds__(MF_THREADS)
 // up to 32 independent loads per lane (4 columns x 8 row blocks) so each warp keeps ~8 KB in flight.
 // ============================================================================================
 constexpr int SOLVE_WARPS = 8;
+constexpr int TOP_PANEL = 2048;  // panels above this (doubles) and their ancestors are swept by a whole CTA
 
 // out[i] = init[i] + sgn * sum_{k<ncols} A[i + k*ld] * xv[k],  i < nrows   (lanes over rows)
-// RB row blocks of 32 per pass and CB = 32/RB columns per batch: 32 independent loads per lane in flight.
+// RB row blocks of 32 per pass and CB = 16/RB columns per batch: 16 independent loads per lane in flight.
 template <int RB>
 __device__ __forceinline__ void warp_gemv_rb(const double* __restrict__ A, int ld, int r0, int nrows, int ncols,
                                              const double* xv, const double* init, double sgn, double* out,
                                              int lane) {
-  constexpr int CB = 32 / RB;
+  constexpr int CB = 16 / RB;
   double acc[RB];
 #pragma unroll
   for (int r = 0; r < RB; ++r) {
@@ -382,13 +443,14 @@ __device__ __forceinline__ void warp_gemv(const double* __restrict__ A, int ld, 
 }
 
 // out[c] = init[c] + sgn * sum_{i<nrows} A[i + c*ld] * xv[i],  c < ncols   (column dot products;
-// lanes over rows, RB row blocks x CB columns of loads per batch, partials reduced through shared
-// memory -- no warp shuffles)
+// lanes over rows, RB row blocks x CB columns of loads per batch; the CB per-lane partials are
+// reduced by a transpose through shared memory: warp shuffles compile to the slow warp-collective
+// sequence inside this persistent loop, whose convergence the compiler cannot prove)
 template <int RB>
 __device__ __forceinline__ void warp_coldot_rb(const double* __restrict__ A, int ld, int nrows, int ncols,
                                                const double* xv, const double* init, double sgn, double* out,
                                                int lane, double* red) {
-  constexpr int CB = 32 / RB;  // columns per batch (<= 32: red holds 32 x 33 doubles)
+  constexpr int CB = 16 / RB;
   for (int c0 = 0; c0 < ncols; c0 += CB) {
     double acc[CB];
 #pragma unroll
@@ -423,7 +485,7 @@ __device__ __forceinline__ void warp_coldot_rb(const double* __restrict__ A, int
 
 __device__ __forceinline__ void warp_coldot(const double* __restrict__ A, int ld, int nrows, int ncols,
                                             const double* xv, const double* init, double sgn, double* out,
-                                            int lane, double* red /* [32 * 33] shared */) {
+                                            int lane, double* red /* [16 * 33] shared */) {
   if (nrows > 64) warp_coldot_rb<4>(A, ld, nrows, ncols, xv, init, sgn, out, lane, red);
   else if (nrows > 32) warp_coldot_rb<2>(A, ld, nrows, ncols, xv, init, sgn, out, lane, red);
   else warp_coldot_rb<1>(A, ld, nrows, ncols, xv, init, sgn, out, lane, red);
@@ -436,113 +498,248 @@ __device__ __forceinline__ int warp_ticket(int* ctr_slot, int lane, volatile int
   return *sh;
 }
 
-// forward solve L y = x (in place, internal order):
-//   v = [x_s; 0] + sum_c ext(u_c);  y = Z v[0:w];  u_s = v[w:m] - L21 y
-__global__ void __launch_bounds__(32 * SOLVE_WARPS)
-    k_fwd_persist(SymDev S, const int32_t* __restrict__ queue, const int32_t* __restrict__ chunk_ptr, int nchunk,
-                  int ns, int* ctr, int* done_all, int B, int epoch, const double* __restrict__ L, int64_t Lsize,
-                  double* X, int n, double* Vb, int64_t Vsize, int max_m, const int* __restrict__ skip,
-                  const int8_t* __restrict__ tiny) {
+// ---------------------------------------------------------------------------------------------
+// Sweeps are two-mode persistent kernels.  The "top" set (large supernodes and all their
+// ancestors; ancestor-closed) is processed one supernode per CTA (8 warps split the rows /
+// columns), everything else one supernode per warp.  Forward: warp mode over the bottom queue,
+// then CTA mode over the top queue; backward: CTA mode first, then warp mode.  Bottom tasks never
+// depend on top tasks in the forward sweep (and vice versa in the backward sweep), so each CTA
+// switches mode exactly once.
+// ---------------------------------------------------------------------------------------------
+struct SweepArgs {
+  const int32_t* queue;      // bottom supernodes, level order
+  const int32_t* chunk_ptr;  // chunks of the bottom queue
+  int nchunk;
+  const int32_t* top;        // top supernodes, level order
+  int ntop;
+  int ns;                    // done-flag stride
+  int* ctr;                  // [4]: warp tickets (2 epoch slots), CTA tickets (2 epoch slots)
+  int* done_all;
+  int B, epoch;
+  const double* L;
+  int64_t Lsize;
+  double* X;
+  int n;
+  double* Vb;
+  int64_t Vsize;
+  int max_m;
+  const int* skip;
+};
+
+__device__ __forceinline__ int cta_ticket(int* ctr_slot, volatile int* sh) {
+  __syncthreads();
+  if (threadIdx.x == 0) *sh = atomicAdd(ctr_slot, 1);
+  __syncthreads();
+  return *sh;
+}
+
+// forward step of supernode s by one warp (v, y: per-warp shared scratch)
+__device__ __forceinline__ void fwd_warp_step(const SymDev& S, const SweepArgs& A, int s, int b, int lane, double* v,
+                                              double* y, ChMeta* cmeta, int* done) {
+  const SnMeta M = S.meta[s];
+  double* x = A.X + (int64_t)b * A.n;
+  const int f = M.f, w = M.w, m = M.m, mu = m - w;
+  const double* P = A.L + b * A.Lsize + M.pofs;
+  for (int i = lane; i < m; i += 32) v[i] = (i < w) ? x[f + i] : 0.0;
+  for (int cb = M.ch0; cb < M.ch1; cb += 32) {
+    const int nc = min(32, M.ch1 - cb);
+    if (lane < nc) {
+      const ChMeta cm = S.chmeta[cb + lane];
+      cmeta[lane] = cm;
+      if (!cm.tiny) wait_epoch(done + cm.c, A.epoch);
+    }
+    __syncwarp();
+    for (int k = 0; k < nc; ++k) {
+      const ChMeta cm = cmeta[k];
+      const double* uc = A.Vb + b * A.Vsize + cm.vofs;
+      const int32_t* rel = S.relmap + cm.relofs;
+      for (int i = lane; i < cm.mc; i += 32) v[__ldg(rel + i)] += __ldcg(uc + i);
+      __syncwarp();
+    }
+  }
+  warp_gemv(P, m, w, w, v, nullptr, 1.0, y, lane);  // y = Z v[0:w]  (Z strict upper part is zero)
+  __syncwarp();
+  for (int i = lane; i < w; i += 32) x[f + i] = y[i];
+  warp_gemv(P + w, m, mu, w, y, v + w, -1.0, A.Vb + b * A.Vsize + M.vofs, lane);
+}
+
+// forward step of a top supernode by the whole CTA (v, y: CTA shared scratch)
+__device__ __forceinline__ void fwd_cta_step(const SymDev& S, const SweepArgs& A, int s, int b, double* v, double* y,
+                                             ChMeta* cmeta, int* done) {
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
+  const SnMeta M = S.meta[s];
+  double* x = A.X + (int64_t)b * A.n;
+  const int f = M.f, w = M.w, m = M.m, mu = m - w;
+  const double* P = A.L + b * A.Lsize + M.pofs;
+  for (int i = tid; i < m; i += nt) v[i] = (i < w) ? x[f + i] : 0.0;
+  for (int cb = M.ch0; cb < M.ch1; cb += 32) {
+    const int nc = min(32, M.ch1 - cb);
+    if (warp == 0 && lane < nc) {
+      const ChMeta cm = S.chmeta[cb + lane];
+      cmeta[lane] = cm;
+      if (!cm.tiny) wait_epoch(done + cm.c, A.epoch);
+    }
+    __syncthreads();
+    for (int k = 0; k < nc; ++k) {
+      const ChMeta cm = cmeta[k];
+      const double* uc = A.Vb + b * A.Vsize + cm.vofs;
+      const int32_t* rel = S.relmap + cm.relofs;
+      for (int i = tid; i < cm.mc; i += nt) v[__ldg(rel + i)] += __ldcg(uc + i);
+      __syncthreads();
+    }
+  }
+  for (int r0 = warp * 32; r0 < w; r0 += nwarp * 32) warp_gemv_rb<1>(P, m, r0, w, w, v, nullptr, 1.0, y, lane);
+  __syncthreads();
+  for (int i = tid; i < w; i += nt) x[f + i] = y[i];
+  double* us = A.Vb + b * A.Vsize + M.vofs;
+  for (int r0 = warp * 32; r0 < mu; r0 += nwarp * 32) warp_gemv_rb<1>(P + w, m, r0, mu, w, y, v + w, -1.0, us, lane);
+}
+
+__global__ void __launch_bounds__(32 * SOLVE_WARPS, 3) k_fwd_persist(SymDev S, SweepArgs A) {
   extern __shared__ double smem[];
-  __shared__ int tk_sh[SOLVE_WARPS];
-  if (blockIdx.x == 0 && threadIdx.x == 0) ctr[(epoch + 1) & 1] = 0;
+  __shared__ int tk_sh[SOLVE_WARPS + 1];
+  __shared__ ChMeta cmeta_all[SOLVE_WARPS][32];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // slots of the next launch
+    A.ctr[(A.epoch + 1) & 1] = 0;
+    A.ctr[2 + ((A.epoch + 1) & 1)] = 0;
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double* v = smem + (size_t)warp * (max_m + 64 + 32 * 33);
-  double* y = v + max_m;
-  const int total = nchunk * B;
+  double* v = smem + (size_t)warp * (A.max_m + 64);
+  double* y = v + A.max_m;
+  ChMeta* cmeta = cmeta_all[warp];
+  // warp mode: bottom queue in chunks
   for (;;) {
-    // dynamic tickets over chunks of consecutive supernodes of the topological queue (chunks are
-    // long at the wide bottom levels and single supernodes near the top)
-    const int t = warp_ticket(&ctr[epoch & 1], lane, &tk_sh[warp]);
-    if (t >= total) break;
-    const int ch = t / B, b = t % B;
-    int* done = done_all + (int64_t)b * ns;
-    const bool sk = skip && skip[b];
-    for (int q = chunk_ptr[ch]; q < chunk_ptr[ch + 1]; ++q) {
-      const int s = queue[q];
+    const int t = warp_ticket(&A.ctr[A.epoch & 1], lane, &tk_sh[warp]);
+    if (t >= A.nchunk * A.B) break;
+    const int ch = t / A.B, b = t % A.B;
+    int* done = A.done_all + (int64_t)b * A.ns;
+    const bool sk = A.skip && A.skip[b];
+    for (int q = A.chunk_ptr[ch]; q < A.chunk_ptr[ch + 1]; ++q) {
+      const int s = A.queue[q];
       if (!sk) {
-        if (lane == 0)
-          for (int ci = S.ch_ptr[s]; ci < S.ch_ptr[s + 1]; ++ci)
-            if (!tiny[S.ch_list[ci]]) wait_epoch(done + S.ch_list[ci], epoch);  // tiny ones: previous kernel
-        __syncwarp();
-        double* x = X + (int64_t)b * n;
-        const int f = S.sfirst[s], w = S.sfirst[s + 1] - f;
-        const int m = (int)(S.srowptr[s + 1] - S.srowptr[s]);
-        const int mu = m - w;
-        const double* P = L + b * Lsize + S.pofs[s];
-        for (int i = lane; i < m; i += 32) v[i] = (i < w) ? x[f + i] : 0.0;
-        __syncwarp();
-        for (int ci = S.ch_ptr[s]; ci < S.ch_ptr[s + 1]; ++ci) {
-          const int c = S.ch_list[ci];
-          const int mc = off_rows(S, c);
-          const double* uc = Vb + b * Vsize + S.vofs[c];
-          const int32_t* rel = S.relmap + S.relofs[c];
-          for (int i = lane; i < mc; i += 32) v[rel[i]] += __ldcg(uc + i);
-          __syncwarp();
-        }
-        warp_gemv(P, m, w, w, v, nullptr, 1.0, y, lane);  // y = Z v[0:w]  (Z strict upper part is zero)
-        __syncwarp();
-        for (int i = lane; i < w; i += 32) x[f + i] = y[i];
-        warp_gemv(P + w, m, mu, w, y, v + w, -1.0, Vb + b * Vsize + S.vofs[s], lane);
+        fwd_warp_step(S, A, s, b, lane, v, y, cmeta, done);
         fence_acq_rel();
         __syncwarp();
       }
-      if (lane == 0) st_release(done + s, epoch);
+      if (lane == 0) st_release(done + s, A.epoch);
     }
+  }
+  // CTA mode: top queue
+  double* vc = smem + (size_t)SOLVE_WARPS * (A.max_m + 64);
+  for (;;) {
+    const int t = cta_ticket(&A.ctr[2 + (A.epoch & 1)], &tk_sh[SOLVE_WARPS]);
+    if (t >= A.ntop * A.B) break;
+    const int s = A.top[t / A.B], b = t % A.B;
+    int* done = A.done_all + (int64_t)b * A.ns;
+    if (!(A.skip && A.skip[b])) {
+      fwd_cta_step(S, A, s, b, vc, vc + A.max_m, cmeta_all[0], done);
+      fence_acq_rel();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) st_release(done + s, A.epoch);
   }
 }
 
-// backward solve L^T x = y: x_s = Z^T (y_s - L21^T x_R); the rows below belong to ancestors
-__global__ void __launch_bounds__(32 * SOLVE_WARPS)
-    k_bwd_persist(SymDev S, const int32_t* __restrict__ queue, const int32_t* __restrict__ chunk_ptr, int nchunk,
-                  int ns, int* ctr, int* done_all, int B, int epoch, const double* __restrict__ L, int64_t Lsize,
-                  double* X, int n, int max_m, const int* __restrict__ skip) {
+// backward step of supernode s by one warp: x_s = Z^T (y_s - L21^T x_R)
+__device__ __forceinline__ void bwd_warp_step(const SymDev& S, const SweepArgs& A, int s, int b, int lane, double* xr,
+                                              double* tv, double* red, int* done) {
+  const SnMeta M = S.meta[s];
+  const int p = S.sparent[s];
+  double* x = A.X + (int64_t)b * A.n;
+  const int f = M.f, w = M.w, m = M.m, mu = m - w;
+  const double* P = A.L + b * A.Lsize + M.pofs;
+  for (int i = lane; i < w; i += 32) tv[i] = x[f + i];
+  const unsigned long long t0 = g_debug_ts ? gtimer() : 0ull;
+  if (p >= 0) wait_epoch(done + p, A.epoch);  // all lanes: uniform control flow
+  __syncwarp();
+  const unsigned long long t1 = g_debug_ts ? gtimer() : 0ull;
+  for (int i = lane; i < mu; i += 32) xr[i] = __ldcg(x + __ldg(S.srows + M.r0 + w + i));
+  __syncwarp();
+  warp_coldot(P + w, m, mu, w, xr, tv, -1.0, tv, lane, red);  // t = y - L21^T x_R
+  __syncwarp();
+  warp_coldot(P, m, w, w, tv, nullptr, 1.0, xr, lane, red);   // x_s = Z^T t  (xr reused as output)
+  __syncwarp();
+  for (int i = lane; i < w; i += 32) x[f + i] = xr[i];
+  if (g_debug_ts && lane == 0 && b == 0) {
+    g_debug_ts[4 * s] = t0;
+    g_debug_ts[4 * s + 1] = t1;
+    g_debug_ts[4 * s + 2] = gtimer();
+    g_debug_ts[4 * s + 3] = 0;
+  }
+}
+
+// backward step of a top supernode by the whole CTA: warps split the columns
+__device__ __forceinline__ void bwd_cta_step(const SymDev& S, const SweepArgs& A, int s, int b, double* xr, double* tv,
+                                             double* xo, double* red_warp, int* done) {
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
+  const SnMeta M = S.meta[s];
+  const int p = S.sparent[s];
+  double* x = A.X + (int64_t)b * A.n;
+  const int f = M.f, w = M.w, m = M.m, mu = m - w;
+  const double* P = A.L + b * A.Lsize + M.pofs;
+  for (int i = tid; i < w; i += nt) tv[i] = x[f + i];
+  const unsigned long long t0 = g_debug_ts ? gtimer() : 0ull;
+  if (tid == 0 && p >= 0) wait_epoch(done + p, A.epoch);
+  __syncthreads();
+  const unsigned long long t1 = g_debug_ts ? gtimer() : 0ull;
+  for (int i = tid; i < mu; i += nt) xr[i] = __ldcg(x + __ldg(S.srows + M.r0 + w + i));
+  __syncthreads();
+  const int cpw = (w + nwarp - 1) / nwarp;  // columns per warp
+  const int c0 = warp * cpw, nc = max(0, min(cpw, w - c0));
+  if (nc > 0) warp_coldot(P + w + (int64_t)c0 * m, m, mu, nc, xr, tv + c0, -1.0, tv + c0, lane, red_warp);
+  __syncthreads();
+  if (nc > 0) warp_coldot(P + (int64_t)c0 * m, m, w, nc, tv, nullptr, 1.0, xo + c0, lane, red_warp);
+  __syncthreads();
+  for (int i = tid; i < w; i += nt) x[f + i] = xo[i];
+  if (g_debug_ts && tid == 0 && b == 0) {
+    g_debug_ts[4 * s] = t0;
+    g_debug_ts[4 * s + 1] = t1;
+    g_debug_ts[4 * s + 2] = gtimer();
+    g_debug_ts[4 * s + 3] = 1;
+  }
+}
+
+__global__ void __launch_bounds__(32 * SOLVE_WARPS, 3) k_bwd_persist(SymDev S, SweepArgs A) {
   extern __shared__ double smem[];
-  __shared__ int tk_sh[SOLVE_WARPS];
-  if (blockIdx.x == 0 && threadIdx.x == 0) ctr[(epoch + 1) & 1] = 0;
+  __shared__ int tk_sh[SOLVE_WARPS + 1];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    A.ctr[(A.epoch + 1) & 1] = 0;
+    A.ctr[2 + ((A.epoch + 1) & 1)] = 0;
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double* xr = smem + (size_t)warp * (max_m + 64 + 32 * 33);
-  double* tv = xr + max_m;
+  double* xr = smem + (size_t)warp * (A.max_m + 64 + 16 * 33);
+  double* tv = xr + A.max_m;
   double* red = tv + 64;
-  const int total = nchunk * B;
+  // CTA mode: top queue in reverse level order
+  double* cx = smem + (size_t)SOLVE_WARPS * (A.max_m + 64 + 16 * 33);
   for (;;) {
-    const int t = warp_ticket(&ctr[epoch & 1], lane, &tk_sh[warp]);
-    if (t >= total) break;
-    const int ch = nchunk - 1 - t / B, b = t % B;  // chunks in reverse topological order
-    int* done = done_all + (int64_t)b * ns;
-    const bool sk = skip && skip[b];
-    for (int q = chunk_ptr[ch + 1] - 1; q >= chunk_ptr[ch]; --q) {
-      const int s = queue[q];
+    const int t = cta_ticket(&A.ctr[2 + (A.epoch & 1)], &tk_sh[SOLVE_WARPS]);
+    if (t >= A.ntop * A.B) break;
+    const int s = A.top[A.ntop - 1 - t / A.B], b = t % A.B;
+    int* done = A.done_all + (int64_t)b * A.ns;
+    if (!(A.skip && A.skip[b])) {
+      bwd_cta_step(S, A, s, b, cx, cx + A.max_m, cx + A.max_m + 64, red, done);
+      fence_acq_rel();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) st_release(done + s, A.epoch);
+  }
+  __syncthreads();
+  // warp mode: bottom queue, chunks in reverse topological order
+  for (;;) {
+    const int t = warp_ticket(&A.ctr[A.epoch & 1], lane, &tk_sh[warp]);
+    if (t >= A.nchunk * A.B) break;
+    const int ch = A.nchunk - 1 - t / A.B, b = t % A.B;
+    int* done = A.done_all + (int64_t)b * A.ns;
+    const bool sk = A.skip && A.skip[b];
+    for (int q = A.chunk_ptr[ch + 1] - 1; q >= A.chunk_ptr[ch]; --q) {
+      const int s = A.queue[q];
       if (!sk) {
-        const int p = S.sparent[s];
-        const unsigned long long t0 = gtimer();
-        if (lane == 0 && p >= 0) wait_epoch(done + p, epoch);
-        __syncwarp();
-        const unsigned long long t1 = gtimer();
-        double* x = X + (int64_t)b * n;
-        const int f = S.sfirst[s], w = S.sfirst[s + 1] - f;
-        const int64_t r0 = S.srowptr[s];
-        const int m = (int)(S.srowptr[s + 1] - r0);
-        const int mu = m - w;
-        const double* P = L + b * Lsize + S.pofs[s];
-        for (int i = lane; i < mu; i += 32) xr[i] = __ldcg(x + S.srows[r0 + w + i]);
-        for (int i = lane; i < w; i += 32) tv[i] = x[f + i];
-        __syncwarp();
-        warp_coldot(P + w, m, mu, w, xr, tv, -1.0, tv, lane, red);  // t = y - L21^T x_R
-        __syncwarp();
-        warp_coldot(P, m, w, w, tv, nullptr, 1.0, xr, lane, red);   // x_s = Z^T t  (xr reused as output)
-        __syncwarp();
-        for (int i = lane; i < w; i += 32) x[f + i] = xr[i];
+        bwd_warp_step(S, A, s, b, lane, xr, tv, red, done);
         fence_acq_rel();
         __syncwarp();
-        if (g_debug_ts && lane == 0 && b == 0) {
-          g_debug_ts[4 * s] = t0;
-          g_debug_ts[4 * s + 1] = t1;
-          g_debug_ts[4 * s + 2] = gtimer();
-          g_debug_ts[4 * s + 3] = (unsigned long long)(blockIdx.x * SOLVE_WARPS + warp);
-        }
       }
-      if (lane == 0) st_release(done + s, epoch);
+      if (lane == 0) st_release(done + s, A.epoch);
     }
   }
 }
@@ -631,5 +828,79 @@ __global__ void __launch_bounds__(256)
         x[f + i] = acc;
       }
     }
+  }
+}
+
+// Factor of tiny subtrees: one thread per subtree, nodes in postorder.  The front panel lives in
+// thread-local memory; the update matrices go to Ub and are consumed by the same thread (children)
+// or by the persistent kernel (subtree root) launched afterwards.
+__global__ void __launch_bounds__(128)
+    k_factor_tiny(SymDev S, const int32_t* __restrict__ sub_ptr, const int32_t* __restrict__ sub_nodes, int nsub,
+                  int B, double* L, int64_t Lsize, double* Ub, int64_t Usize, const double* __restrict__ Kval,
+                  int64_t nnzk, int* notpd, int* minpiv) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nsub * B) return;
+  const int sub = t / B, b = t % B;
+  const double* Kb = Kval + b * nnzk;
+  double* Ubb = Ub + b * Usize;
+  for (int q = sub_ptr[sub]; q < sub_ptr[sub + 1]; ++q) {
+    const int s = sub_nodes[q];
+    const int f = S.sfirst[s], w = S.sfirst[s + 1] - f;
+    const int m = (int)(S.srowptr[s + 1] - S.srowptr[s]);
+    const int mu = m - w;
+    double P[TINY_M * TINY_W];
+    for (int i = 0; i < m * w; ++i) P[i] = 0.0;
+    for (int64_t k = S.kp[f]; k < S.kp[f + w]; ++k) P[S.kmap[k]] = Kb[k];
+    for (int ci = S.ch_ptr[s]; ci < S.ch_ptr[s + 1]; ++ci) {  // panel part of the children
+      const int c = S.ch_list[ci];
+      const int mc = off_rows(S, c);
+      const double* Uc = Ubb + S.uofs[c];
+      const int32_t* rel = S.relmap + S.relofs[c];
+      for (int j = 0; j < mc && rel[j] < w; ++j)
+        for (int i = j; i < mc; ++i) P[rel[i] + rel[j] * m] += Uc[i + j * mc];
+    }
+    for (int j = 0; j < w; ++j) {  // Cholesky of the first w columns
+      double d = P[j + j * m];
+      if (!(d > 0.0) || !isfinite(d)) {
+        notpd[b] = 1;
+        atomicMin(&minpiv[b], f + j);
+        d = nan("");
+      }
+      const double piv = sqrt(d);
+      P[j + j * m] = piv;
+      for (int i = j + 1; i < m; ++i) P[i + j * m] /= piv;
+      for (int c2 = j + 1; c2 < w; ++c2) {
+        const double lc = P[c2 + j * m];
+        for (int i = c2; i < m; ++i) P[i + c2 * m] -= P[i + j * m] * lc;
+      }
+    }
+    double* U = Ubb + S.uofs[s];
+    for (int j = 0; j < mu; ++j)  // U_s = -L21 L21^T (lower)
+      for (int i = j; i < mu; ++i) {
+        double acc = 0.0;
+        for (int k = 0; k < w; ++k) acc += P[w + i + k * m] * P[w + j + k * m];
+        U[i + j * mu] = -acc;
+      }
+    for (int ci = S.ch_ptr[s]; ci < S.ch_ptr[s + 1]; ++ci) {  // trailing part of the children
+      const int c = S.ch_list[ci];
+      const int mc = off_rows(S, c);
+      const double* Uc = Ubb + S.uofs[c];
+      const int32_t* rel = S.relmap + S.relofs[c];
+      for (int j = 0; j < mc; ++j) {
+        if (rel[j] < w) continue;
+        for (int i = j; i < mc; ++i) U[(rel[i] - w) + (rel[j] - w) * mu] += Uc[i + j * mc];
+      }
+    }
+    for (int i = 0; i < w; ++i) {  // L11 <- L11^{-1}, row by row
+      double z[TINY_W];
+      for (int j = 0; j <= i; ++j) {
+        double acc = (j == i) ? 1.0 : 0.0;
+        for (int k = j; k < i; ++k) acc -= P[i + k * m] * P[k + j * m];
+        z[j] = acc / P[i + i * m];
+      }
+      for (int j = 0; j <= i; ++j) P[i + j * m] = z[j];
+    }
+    double* Pg = L + b * Lsize + S.pofs[s];
+    for (int i = 0; i < m * w; ++i) Pg[i] = P[i];
   }
 }
