@@ -259,6 +259,9 @@ def run_ckkt(args, world, rank, local):
             "avg_launch_ms": avg,
             "phases_ms_per_step": {k: v[0] / args.steps for k, v in phases.items()},
             "launches_per_step": {k: v[1] / args.steps for k, v in phases.items()}}
+    tr_path = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tr_path):  # DRAM bytes per launch of this kernel from the committed ncu capture
+        roof["traffic"] = json.load(open(tr_path)).get(roof["kernel"])
     fac_ms = phases["factor"][0] / max(phases["factor"][1], 1)
     fp64 = {"kernel": "k_factor_persist", "flops": sizes["flops_factor"], "ms": fac_ms,
             "achieved_tflops": sizes["flops_factor"] / (fac_ms * 1e-3) / 1e12, "peak_tflops": 37.1,
