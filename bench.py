@@ -29,7 +29,7 @@ CONFIGS = {
     "c1": (50, 1, "distillation column N=50, single KKT system"),
     "c2": (1000, 1, "distillation column N=1000, single KKT system, 18-iterate trajectory"),
     "c3": (50000, 1, "distillation column N=50000 (largest in PAPER.md Table I), single system per GPU"),
-    "c4": (1000, 64, "batch of 64 NMPC instances N=1000 (per GPU)"),
+    "c4": (1000, 64, "batch of 64 NMPC instances N=1000 sharded over the GPUs"),
 }
 
 
@@ -97,27 +97,24 @@ def dist_init():
     return world, rank, local
 
 
-def build_inputs(N, instance, dev, T_iter=18):
+def build_inputs(N, instances, dev):
+    """Values of the 18-iterate trajectories of the given instances, stacked [T, B, len] on `dev`."""
     import numpy as np
     import torch
     from inputs import distillation as dist
-    inst = dist.Instance(N, instance)
-    traj = inst.trajectory()
-    pat = inst.model.pat
+    insts = [dist.Instance(N, i) for i in instances]
+    trajs = [inst.trajectory() for inst in insts]
+    pat = insts[0].model.pat
     n, m = pat.n, pat.m
-    rng = np.random.default_rng(3000 + instance)
-    data = {
-        "pat": pat, "n": n, "m": m,
-        "w": torch.as_tensor(np.stack([it.w_val for it in traj]), device=dev),
-        "j": torch.as_tensor(np.stack([it.j_val for it in traj]), device=dev),
-        "sig": torch.as_tensor(np.stack([it.sigma_x for it in traj]), device=dev),
-        "dl": torch.as_tensor(np.stack([it.d_lifted for it in traj]), device=dev),
-        "r1": torch.as_tensor(rng.standard_normal((len(traj), n)), device=dev),
-        "ra": torch.as_tensor(rng.standard_normal((len(traj), m)), device=dev),
-        "rb": torch.as_tensor(rng.standard_normal((len(traj), m)), device=dev),
-        "traj": traj, "inst": inst,
-    }
-    return data
+    T = len(trajs[0])
+    rngs = [np.random.default_rng(3000 + i) for i in instances]
+    st = lambda f: torch.as_tensor(np.stack([np.stack([getattr(tr[k], f) for tr in trajs]) for k in range(T)]),
+                                   device=dev)
+    rhs = lambda cols: torch.as_tensor(np.stack([np.stack([r.standard_normal(cols) for r in rngs]) for _ in range(T)]),
+                                       device=dev)
+    return {"pat": pat, "n": n, "m": m, "B": len(instances),
+            "w": st("w_val"), "j": st("j_val"), "sig": st("sigma_x"), "dl": st("d_lifted"),
+            "r1": rhs(n), "ra": rhs(m), "rb": rhs(m)}
 
 
 def run_ckkt(args, world, rank, local):
@@ -129,20 +126,25 @@ def run_ckkt(args, world, rank, local):
     if world > 1:
         import torch.distributed as tdist
         tdist.init_process_group("nccl", device_id=dev)
+    from paper_2403_15913_b200.sharding import max_over_ranks, per_unit_ms, shard
     N, batch, desc = CONFIGS[args.config]
     t0 = time.time()
-    data = build_inputs(N, rank, dev)
-    pat, n, m = data["pat"], data["n"], data["m"]
+    # config 4 shards a fixed batch of instances over the ranks (strong scaling); the single-system
+    # configs give every rank its own instance (weak scaling)
+    mine = list(shard(batch, world, rank)) if batch > 1 else [rank]
+    total_units = batch if batch > 1 else world
+    data = build_inputs(N, mine, dev)
+    pat, n, m, B = data["pat"], data["n"], data["m"], data["B"]
     T = data["w"].shape[0]
     stream = torch.cuda.current_stream()
     t1 = time.time()
     ctx = ckkt.Context(n, m, 0, pat.w_row, pat.w_col, pat.j_rowptr, pat.j_col, None, None, strategy=ckkt.CKKT_HYKKT,
-                       leaf=args.leaf, device=local, stream=stream.cuda_stream)
+                       leaf=args.leaf, batch=B, device=local, stream=stream.cuda_stream)
     setup_s = time.time() - t1
     sizes = ctx.get_sizes()
-    dx = torch.empty(n, dtype=torch.float64, device=dev)
-    dy = torch.empty(m, dtype=torch.float64, device=dev)
-    notpd = torch.zeros(1, dtype=torch.int32, device=dev)
+    dx = torch.empty((B, n), dtype=torch.float64, device=dev)
+    dy = torch.empty((B, m), dtype=torch.float64, device=dev)
+    notpd = torch.zeros(B, dtype=torch.int32, device=dev)
 
     def step(k, c=ctx):
         c.refactor(data["w"][k], data["j"][k], None, data["sig"][k], None, None, notpd, None)
@@ -163,26 +165,21 @@ def run_ckkt(args, world, rank, local):
         ev0.record(stream)
         for k in range(args.steps):
             rc, info = step((args.warmup + k) % T)
-            infos.append(info[0])
+            infos.extend(info)
         ev1.record(stream)
         torch.cuda.synchronize()
     launches = ctx.launch_count() - l0
     phases = ctx.phase_times()
     ctx.profile(False)
-    ms = ev0.elapsed_time(ev1)
-    if world > 1:
-        import torch.distributed as tdist
-        t = torch.tensor([ms], device=dev)
-        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-        tdist.barrier()
-        ms = float(t.item())
+    ms = max_over_ranks(ev0.elapsed_time(ev1), dev)
     # Lifted-KKT on the same instance (extra key)
     lifted = None
     if not args.no_lifted:
         ctxl = ckkt.Context(n, 0, m, pat.w_row, pat.w_col, None, None, pat.j_rowptr, pat.j_col,
-                            strategy=ckkt.CKKT_LIFTED, leaf=args.leaf, device=local, stream=stream.cuda_stream)
-        ds = torch.empty(m, dtype=torch.float64, device=dev)
-        dz = torch.empty(m, dtype=torch.float64, device=dev)
+                            strategy=ckkt.CKKT_LIFTED, leaf=args.leaf, batch=B, device=local,
+                            stream=stream.cuda_stream)
+        ds = torch.empty((B, m), dtype=torch.float64, device=dev)
+        dz = torch.empty((B, m), dtype=torch.float64, device=dev)
 
         def lstep(k):
             ctxl.refactor(data["w"][k], None, data["j"][k], data["sig"][k], data["dl"][k], None, notpd, None)
@@ -194,10 +191,10 @@ def run_ckkt(args, world, rank, local):
         linfo = []
         ev0.record(stream)
         for k in range(args.steps):
-            linfo.append(lstep((args.warmup + k) % T)[1][0])
+            linfo.extend(lstep((args.warmup + k) % T)[1])
         ev1.record(stream)
         torch.cuda.synchronize()
-        lifted = {"ms_per_iter": ev0.elapsed_time(ev1) / args.steps,
+        lifted = {"ms_per_iter": per_unit_ms(max_over_ranks(ev0.elapsed_time(ev1), dev), args.steps, total_units),
                   "n_ref_mean": float(np.mean([i["n_ref"] for i in linfo])),
                   "rel_res_max": float(max(i["rel_res"] for i in linfo)),
                   "rel_res_unrefined_max": float(max(i["rel_res_unrefined"] for i in linfo)),
@@ -211,8 +208,8 @@ def run_ckkt(args, world, rank, local):
         hs = data["sig"].cpu().pin_memory()
         hr1 = data["r1"].cpu().pin_memory()
         hra = data["ra"].cpu().pin_memory()
-        hdx = torch.empty(n, dtype=torch.float64).pin_memory()
-        hdy = torch.empty(m, dtype=torch.float64).pin_memory()
+        hdx = torch.empty((B, n), dtype=torch.float64).pin_memory()
+        hdy = torch.empty((B, m), dtype=torch.float64).pin_memory()
         for k in range(args.warmup):
             ctx.iterate_host(hw[k], hj[k], None, hs[k], None, None, hr1[k], None, hra[k], None, hdx, None, hdy, None)
         torch.cuda.synchronize()
@@ -223,16 +220,11 @@ def run_ckkt(args, world, rank, local):
                              None)
         ev1.record(stream)
         torch.cuda.synchronize()
-        e_ms = ev0.elapsed_time(ev1)
-        if world > 1:
-            import torch.distributed as tdist
-            t = torch.tensor([e_ms], device=dev)
-            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-            e_ms = float(t.item())
-        h2d = 8 * (hw.shape[1] + hj.shape[1] + hs.shape[1] + hr1.shape[1] + hra.shape[1])
-        d2h = 8 * (n + m)
-        e2e = {"value": e_ms / (args.steps * world), "unit": "ms/IPM-iter", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h}
+        e_ms = max_over_ranks(ev0.elapsed_time(ev1), dev)
+        h2d = 8 * B * (hw.shape[-1] + hj.shape[-1] + hs.shape[-1] + hr1.shape[-1] + hra.shape[-1])
+        d2h = 8 * B * (n + m)
+        e2e = {"value": per_unit_ms(e_ms, args.steps, total_units), "unit": "ms/IPM-iter",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
     if rank != 0:
         if world > 1:
             torch.distributed.destroy_process_group()
@@ -243,9 +235,9 @@ def run_ckkt(args, world, rank, local):
     #   forward / backward sweep: read every panel once + read/write x   = 8 (l_storage + 2 n)
     #   factorization:            read K, write L                        = 8 (nnz_k + l_storage)
     #   condensation:             read W, J, Sigma, maps; write K
-    algo = {"forward": 8.0 * (sizes["l_storage"] + 2 * n), "backward": 8.0 * (sizes["l_storage"] + 2 * n),
-            "factor": 8.0 * (sizes["nnz_k"] + sizes["l_storage"]),
-            "condense": 8.0 * (len(pat.w_row) + len(pat.j_col) + n + sizes["nnz_k"])}
+    algo = {"forward": 8.0 * B * (sizes["l_storage"] + 2 * n), "backward": 8.0 * B * (sizes["l_storage"] + 2 * n),
+            "factor": 8.0 * B * (sizes["nnz_k"] + sizes["l_storage"]),
+            "condense": 8.0 * B * (len(pat.w_row) + len(pat.j_col) + n + sizes["nnz_k"])}
     dom = max(phases, key=lambda k: phases[k][0])
     dom_ms, dom_n = phases[dom]
     avg = dom_ms / max(dom_n, 1)
@@ -263,8 +255,8 @@ def run_ckkt(args, world, rank, local):
     if os.path.exists(tr_path):  # DRAM bytes per launch of this kernel from the committed ncu capture
         roof["traffic"] = json.load(open(tr_path)).get(roof["kernel"])
     fac_ms = phases["factor"][0] / max(phases["factor"][1], 1)
-    fp64 = {"kernel": "k_factor_persist", "flops": sizes["flops_factor"], "ms": fac_ms,
-            "achieved_tflops": sizes["flops_factor"] / (fac_ms * 1e-3) / 1e12, "peak_tflops": 37.1,
+    fp64 = {"kernel": "k_factor_persist", "flops": B * sizes["flops_factor"], "ms": fac_ms,
+            "achieved_tflops": B * sizes["flops_factor"] / (fac_ms * 1e-3) / 1e12, "peak_tflops": 37.1,
             "peak_source": "measured DFMA/DMMA microbenchmark, profiles/fp64_peak_r01.txt"}
     fp64["frac"] = fp64["achieved_tflops"] / fp64["peak_tflops"]
     cpu = None
@@ -277,16 +269,17 @@ def run_ckkt(args, world, rank, local):
                     "status_max": int(max(i["status"] for i in infos))}
     out = {
         "metric": "KKT refactor+solve ms/IPM-iter (FP64)",
-        "value": ms / (args.steps * world),
+        "value": per_unit_ms(ms, args.steps, total_units),
         "unit": "ms/IPM-iter",
         "higher_is_better": False,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps,
-        "scaling": "weak",
+        "scaling": "strong" if batch > 1 else "weak",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic distillation-column IPM iterates (inputs/distillation.py), random N(0,1) rhs",
         "config": {"workload": desc, "N": N, "n": n, "m_e": m, "strategy": "HyKKT gamma=1e7",
+                   "instances_per_gpu": B, "units": "one IPM iteration of one KKT system",
                    "leaf": args.leaf, "l2": "inputs larger than L2 (L factor %.2f GB)" % (sizes["l_storage"] * 8 / 1e9),
                    "parallelism": f"replicas x{world}"},
         "phases_ms": {"refactor": (phases["condense"][0] + phases["factor"][0]) / args.steps,
