@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libckkt.so")
+LIB_PATH = os.environ.get("CKKT_LIB_OVERRIDE") or os.path.join(_HERE, "libckkt.so")  # override: experiments only
 
 CKKT_OK, CKKT_NOT_PD, CKKT_CG_NO_CONVERGENCE, CKKT_REFINE_NOT_CONVERGED = 0, 1, 2, 3
 CKKT_PATTERN_ERROR, CKKT_INVALID_ARG, CKKT_CUDA_ERROR, CKKT_OUT_OF_MEMORY = 4, 5, 6, 7

@@ -736,9 +736,11 @@ ckkt_status setup_device(ckkt_ctx* c) {
       c->tinyflag = upload(T, o, by);
       // top set: large supernodes (panel > TOP_PANEL doubles) and all their ancestors (one CTA each)
       std::vector<int8_t> top(ns, 0);
+      int64_t top_panel = TOP_PANEL;
+      if (const char* e = getenv("CKKT_TOP_PANEL")) top_panel = atoll(e);  // tuning experiments
       for (int s2 = 0; s2 < ns; ++s2) {
         const int64_t m = A.srowptr[s2 + 1] - A.srowptr[s2], w = A.sfirst[s2 + 1] - A.sfirst[s2];
-        if (!T[s2] && m * w > TOP_PANEL) top[s2] = 1;
+        if (!T[s2] && m * w > top_panel) top[s2] = 1;
       }
       for (int s2 = 0; s2 < ns; ++s2)  // postorder: parents after children
         if (top[s2] && A.sparent[s2] >= 0) top[A.sparent[s2]] = 1;
@@ -1488,7 +1490,9 @@ extern "C" int ckkt_debug_trace_bwd(ckkt_ctx* c, unsigned long long* host_ts) {
   cudaMemset(d, 0, sizeof(unsigned long long) * 4 * c->A.ns);
   cudaMemcpyToSymbol(g_debug_ts, &d, sizeof(d));
   unsigned long long* dph = nullptr;
-  if (getenv("CKKT_TRACE_FACTOR")) {
+  if (getenv("CKKT_TRACE_FWD")) {
+    launch_fwd(c, c->tn, nullptr);
+  } else if (getenv("CKKT_TRACE_FACTOR")) {
     cudaMalloc(&dph, sizeof(unsigned long long) * 8 * c->A.ns);
     cudaMemset(dph, 0, sizeof(unsigned long long) * 8 * c->A.ns);
     cudaMemcpyToSymbol(g_debug_ph, &dph, sizeof(dph));

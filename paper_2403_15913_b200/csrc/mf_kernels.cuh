@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(MF_THREADS)
 // up to 32 independent loads per lane (4 columns x 8 row blocks) so each warp keeps ~8 KB in flight.
 // ============================================================================================
 constexpr int SOLVE_WARPS = 8;
-constexpr int TOP_PANEL = 2048;  // panels above this (doubles) and their ancestors are swept by a whole CTA
+constexpr int TOP_PANEL = 4096;  // panels above this (doubles) and their ancestors are swept by a whole CTA
 
 // out[i] = init[i] + sgn * sum_{k<ncols} A[i + k*ld] * xv[k],  i < nrows   (lanes over rows)
 // RB row blocks of 32 per pass and CB = 16/RB columns per batch: 16 independent loads per lane in flight.
@@ -540,6 +540,7 @@ __device__ __forceinline__ void fwd_warp_step(const SymDev& S, const SweepArgs& 
   double* x = A.X + (int64_t)b * A.n;
   const int f = M.f, w = M.w, m = M.m, mu = m - w;
   const double* P = A.L + b * A.Lsize + M.pofs;
+  const unsigned long long t0 = g_debug_ts ? gtimer() : 0ull;
   for (int i = lane; i < m; i += 32) v[i] = (i < w) ? x[f + i] : 0.0;
   for (int cb = M.ch0; cb < M.ch1; cb += 32) {
     const int nc = min(32, M.ch1 - cb);
@@ -561,6 +562,12 @@ __device__ __forceinline__ void fwd_warp_step(const SymDev& S, const SweepArgs& 
   __syncwarp();
   for (int i = lane; i < w; i += 32) x[f + i] = y[i];
   warp_gemv(P + w, m, mu, w, y, v + w, -1.0, A.Vb + b * A.Vsize + M.vofs, lane);
+  if (g_debug_ts && lane == 0 && b == 0) {
+    g_debug_ts[4 * s] = t0;
+    g_debug_ts[4 * s + 1] = t0;
+    g_debug_ts[4 * s + 2] = gtimer();
+    g_debug_ts[4 * s + 3] = 0;
+  }
 }
 
 // forward step of a top supernode by the whole CTA (v, y: CTA shared scratch)
@@ -571,6 +578,7 @@ __device__ __forceinline__ void fwd_cta_step(const SymDev& S, const SweepArgs& A
   double* x = A.X + (int64_t)b * A.n;
   const int f = M.f, w = M.w, m = M.m, mu = m - w;
   const double* P = A.L + b * A.Lsize + M.pofs;
+  const unsigned long long t0 = g_debug_ts ? gtimer() : 0ull;
   for (int i = tid; i < m; i += nt) v[i] = (i < w) ? x[f + i] : 0.0;
   for (int cb = M.ch0; cb < M.ch1; cb += 32) {
     const int nc = min(32, M.ch1 - cb);
@@ -593,6 +601,12 @@ __device__ __forceinline__ void fwd_cta_step(const SymDev& S, const SweepArgs& A
   for (int i = tid; i < w; i += nt) x[f + i] = y[i];
   double* us = A.Vb + b * A.Vsize + M.vofs;
   for (int r0 = warp * 32; r0 < mu; r0 += nwarp * 32) warp_gemv_rb<1>(P + w, m, r0, mu, w, y, v + w, -1.0, us, lane);
+  if (g_debug_ts && tid == 0 && b == 0) {
+    g_debug_ts[4 * s] = t0;
+    g_debug_ts[4 * s + 1] = t0;
+    g_debug_ts[4 * s + 2] = gtimer();
+    g_debug_ts[4 * s + 3] = 1;
+  }
 }
 
 __global__ void __launch_bounds__(32 * SOLVE_WARPS, 3) k_fwd_persist(SymDev S, SweepArgs A) {
@@ -750,7 +764,13 @@ __global__ void __launch_bounds__(32 * SOLVE_WARPS, 3) k_bwd_persist(SymDev S, S
 // kernel, backward after it, so no flags are needed: every dependency outside the subtree was
 // completed by the other launch, every dependency inside it by the same thread.
 // ============================================================================================
-constexpr int TINY_M = 32, TINY_W = 4;
+#ifndef CKKT_TINY_M
+#define CKKT_TINY_M 32
+#endif
+#ifndef CKKT_TINY_W
+#define CKKT_TINY_W 4
+#endif
+constexpr int TINY_M = CKKT_TINY_M, TINY_W = CKKT_TINY_W;
 
 __global__ void __launch_bounds__(256)
     k_fwd_tiny(SymDev S, const int32_t* __restrict__ sub_ptr, const int32_t* __restrict__ sub_nodes, int nsub, int B,

@@ -48,7 +48,11 @@ for lo, hi in [(0, 2000), (2000, 5000), (5000, 10000), (10000, 1e9)]:
     ss = sel & (m * w >= lo) & (m * w < hi)
     if ss.any(): print(f"panel [{lo},{hi}) n={ss.sum()} mean proc {proc[ss].mean():.1f} us")
 ph = np.fromfile('/tmp/ckkt_phases.bin', dtype=np.uint64).reshape(ns, 8).astype(np.float64)
-sel = ph[:, 0] > 0
+issmall = ph[:, 7] == 1
+sel = (ph[:, 0] > 0) & issmall
+d = np.diff(ph[sel][:, :7], axis=1) / 1e3
+print('SMALL fronts:', sel.sum(), ' '.join(f"{nm}={d[:, k].mean():.1f}" for k, nm in enumerate(['zero+K', 'ext-panel', 'dense', 'syrk+out', '-', 'ext-U'])))
+sel = (ph[:, 0] > 0) & ~issmall
 d = np.diff(ph[sel][:, :7], axis=1) / 1e3
 names = ['zero+K', 'ext-panel', 'dense', 'syrk', 'panel-out', 'ext-U']
 pw = (m * w)[sel]
