@@ -672,7 +672,8 @@ ckkt_status setup_device(ckkt_ctx* c) {
     c->Qfwd = Sched{c->ntask, d_tsn, d_tbig, dfwd, cfwd};
     c->Qbwd = Sched{c->ntask, d_tsn, d_tbig, dbwd, cbwd};
     c->fac_smem = std::max<int64_t>(c->big_smem, 8 * SMALL_WARPS * SMALL_PANEL);
-    c->sol_smem = 8 * ((int64_t)SOLVE_WARPS * (c->max_m + 64 + 16 * 33) + c->max_m + 128);
+    c->sol_smem = 8 * ((int64_t)SOLVE_WARPS * (c->max_m + 64 + 16 * 33) + c->max_m + 128) +
+                  4 * (int64_t)SOLVE_WARPS * c->max_m;  // + per-warp row indices (backward)
     if (c->fac_smem > 227 * 1024 || c->sol_smem > 227 * 1024) return CKKT_INVALID_ARG;
     CK(cudaFuncSetAttribute(k_factor_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->fac_smem));
     CK(cudaFuncSetAttribute(k_fwd_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->sol_smem));
@@ -1141,8 +1142,6 @@ void launch_bwd(ckkt_ctx* c, double* x, const int* skip) {
 
 // x <- K^{-1} x  (internal order, in place), skipping instances with skip[b]
 void ksolve(ckkt_ctx* c, double* x, const int* skip) {
-  const auto& A = c->A;
-  cudaStream_t st = c->stream;
   launch_fwd(c, x, skip);
   launch_bwd(c, x, skip);
   c->launches += 2 * ((c->nq > 0) + (c->nsub > 0));
@@ -1452,7 +1451,6 @@ extern "C" int ckkt_debug_time(ckkt_ctx* c, int reps, double* out) {
     cudaMemcpyToSymbol(g_debug_nowait, &nw, sizeof(int));
   }
   cudaStream_t st = c->stream;
-  const auto& A = c->A;
   cudaEvent_t e0, e1, e2;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);

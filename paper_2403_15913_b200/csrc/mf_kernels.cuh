@@ -88,13 +88,16 @@ __device__ __forceinline__ int ld_relaxed(const int* p) {
   return v;
 }
 
+#ifndef CKKT_POLL_MAX_NS
+#define CKKT_POLL_MAX_NS 256
+#endif
 // poll with relaxed loads, then one acquire fence (cheaper than repeated ld.acquire)
 __device__ __forceinline__ void wait_epoch(const int* p, int epoch) {
   if (g_debug_nowait) return;
   int ns = 32;
   while (ld_relaxed(p) != epoch) {
     __nanosleep(ns);
-    ns = ns < 2048 ? 2 * ns : 2048;
+    ns = ns < CKKT_POLL_MAX_NS ? 2 * ns : CKKT_POLL_MAX_NS;
   }
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
@@ -111,6 +114,9 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
 
 // TMA bulk prefetch of [p, p + bytes) into L2 (fire and forget; 16-byte granularity)
 __device__ __forceinline__ void prefetch_l2(const void* p, int64_t bytes) {
+#ifdef CKKT_NO_PREFETCH
+  return;
+#endif
   uintptr_t a = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
   const uintptr_t e = (reinterpret_cast<uintptr_t>(p) + bytes + 15) & ~uintptr_t(15);
   while (a < e) {
@@ -394,6 +400,10 @@ __global__ void __launch_bounds__(MF_THREADS)
 // up to 32 independent loads per lane (4 columns x 8 row blocks) so each warp keeps ~8 KB in flight.
 // ============================================================================================
 constexpr int SOLVE_WARPS = 8;
+#ifndef CKKT_SOLVE_MINB
+#define CKKT_SOLVE_MINB 3
+#endif
+constexpr int SOLVE_MINB = CKKT_SOLVE_MINB;  // resident CTAs per SM the register budget is sized for
 constexpr int TOP_PANEL = 4096;  // panels above this (doubles) and their ancestors are swept by a whole CTA
 
 // out[i] = init[i] + sgn * sum_{k<ncols} A[i + k*ld] * xv[k],  i < nrows   (lanes over rows)
@@ -540,6 +550,7 @@ __device__ __forceinline__ void fwd_warp_step(const SymDev& S, const SweepArgs& 
   double* x = A.X + (int64_t)b * A.n;
   const int f = M.f, w = M.w, m = M.m, mu = m - w;
   const double* P = A.L + b * A.Lsize + M.pofs;
+  if (lane == 0) prefetch_l2(P, 8ll * m * w);  // the panel streams into L2 while the children are gathered
   const unsigned long long t0 = g_debug_ts ? gtimer() : 0ull;
   for (int i = lane; i < m; i += 32) v[i] = (i < w) ? x[f + i] : 0.0;
   for (int cb = M.ch0; cb < M.ch1; cb += 32) {
@@ -578,6 +589,7 @@ __device__ __forceinline__ void fwd_cta_step(const SymDev& S, const SweepArgs& A
   double* x = A.X + (int64_t)b * A.n;
   const int f = M.f, w = M.w, m = M.m, mu = m - w;
   const double* P = A.L + b * A.Lsize + M.pofs;
+  if (tid == 0) prefetch_l2(P, 8ll * m * w);
   const unsigned long long t0 = g_debug_ts ? gtimer() : 0ull;
   for (int i = tid; i < m; i += nt) v[i] = (i < w) ? x[f + i] : 0.0;
   for (int cb = M.ch0; cb < M.ch1; cb += 32) {
@@ -609,7 +621,7 @@ __device__ __forceinline__ void fwd_cta_step(const SymDev& S, const SweepArgs& A
   }
 }
 
-__global__ void __launch_bounds__(32 * SOLVE_WARPS, 3) k_fwd_persist(SymDev S, SweepArgs A) {
+__global__ void __launch_bounds__(32 * SOLVE_WARPS, SOLVE_MINB) k_fwd_persist(SymDev S, SweepArgs A) {
   extern __shared__ double smem[];
   __shared__ int tk_sh[SOLVE_WARPS + 1];
   __shared__ ChMeta cmeta_all[SOLVE_WARPS][32];
@@ -632,7 +644,6 @@ __global__ void __launch_bounds__(32 * SOLVE_WARPS, 3) k_fwd_persist(SymDev S, S
       const int s = A.queue[q];
       if (!sk) {
         fwd_warp_step(S, A, s, b, lane, v, y, cmeta, done);
-        fence_acq_rel();
         __syncwarp();
       }
       if (lane == 0) st_release(done + s, A.epoch);
@@ -647,7 +658,6 @@ __global__ void __launch_bounds__(32 * SOLVE_WARPS, 3) k_fwd_persist(SymDev S, S
     int* done = A.done_all + (int64_t)b * A.ns;
     if (!(A.skip && A.skip[b])) {
       fwd_cta_step(S, A, s, b, vc, vc + A.max_m, cmeta_all[0], done);
-      fence_acq_rel();
     }
     __syncthreads();
     if (threadIdx.x == 0) st_release(done + s, A.epoch);
@@ -656,18 +666,20 @@ __global__ void __launch_bounds__(32 * SOLVE_WARPS, 3) k_fwd_persist(SymDev S, S
 
 // backward step of supernode s by one warp: x_s = Z^T (y_s - L21^T x_R)
 __device__ __forceinline__ void bwd_warp_step(const SymDev& S, const SweepArgs& A, int s, int b, int lane, double* xr,
-                                              double* tv, double* red, int* done) {
+                                              double* tv, double* red, int* ridx, int* done) {
   const SnMeta M = S.meta[s];
   const int p = S.sparent[s];
   double* x = A.X + (int64_t)b * A.n;
   const int f = M.f, w = M.w, m = M.m, mu = m - w;
   const double* P = A.L + b * A.Lsize + M.pofs;
+  if (lane == 0) prefetch_l2(P, 8ll * m * w);  // independent of the parent: overlap with the wait
   for (int i = lane; i < w; i += 32) tv[i] = x[f + i];
+  for (int i = lane; i < mu; i += 32) ridx[i] = __ldg(S.srows + M.r0 + w + i);
   const unsigned long long t0 = g_debug_ts ? gtimer() : 0ull;
   if (p >= 0) wait_epoch(done + p, A.epoch);  // all lanes: uniform control flow
   __syncwarp();
   const unsigned long long t1 = g_debug_ts ? gtimer() : 0ull;
-  for (int i = lane; i < mu; i += 32) xr[i] = __ldcg(x + __ldg(S.srows + M.r0 + w + i));
+  for (int i = lane; i < mu; i += 32) xr[i] = __ldcg(x + ridx[i]);
   __syncwarp();
   warp_coldot(P + w, m, mu, w, xr, tv, -1.0, tv, lane, red);  // t = y - L21^T x_R
   __syncwarp();
@@ -691,12 +703,19 @@ __device__ __forceinline__ void bwd_cta_step(const SymDev& S, const SweepArgs& A
   double* x = A.X + (int64_t)b * A.n;
   const int f = M.f, w = M.w, m = M.m, mu = m - w;
   const double* P = A.L + b * A.Lsize + M.pofs;
+  if (tid == 0) prefetch_l2(P, 8ll * m * w);
   for (int i = tid; i < w; i += nt) tv[i] = x[f + i];
+  int ri[4];  // row indices of this thread (mu <= 4 * blockDim), loaded before the wait
+#pragma unroll
+  for (int k = 0; k < 4; ++k) ri[k] = (tid + k * nt < mu) ? __ldg(S.srows + M.r0 + w + tid + k * nt) : 0;
   const unsigned long long t0 = g_debug_ts ? gtimer() : 0ull;
   if (tid == 0 && p >= 0) wait_epoch(done + p, A.epoch);
   __syncthreads();
   const unsigned long long t1 = g_debug_ts ? gtimer() : 0ull;
-  for (int i = tid; i < mu; i += nt) xr[i] = __ldcg(x + __ldg(S.srows + M.r0 + w + i));
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (tid + k * nt < mu) xr[tid + k * nt] = __ldcg(x + ri[k]);
+  for (int i = tid + 4 * nt; i < mu; i += nt) xr[i] = __ldcg(x + __ldg(S.srows + M.r0 + w + i));
   __syncthreads();
   const int cpw = (w + nwarp - 1) / nwarp;  // columns per warp
   const int c0 = warp * cpw, nc = max(0, min(cpw, w - c0));
@@ -713,7 +732,7 @@ __device__ __forceinline__ void bwd_cta_step(const SymDev& S, const SweepArgs& A
   }
 }
 
-__global__ void __launch_bounds__(32 * SOLVE_WARPS, 3) k_bwd_persist(SymDev S, SweepArgs A) {
+__global__ void __launch_bounds__(32 * SOLVE_WARPS, SOLVE_MINB) k_bwd_persist(SymDev S, SweepArgs A) {
   extern __shared__ double smem[];
   __shared__ int tk_sh[SOLVE_WARPS + 1];
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -724,6 +743,8 @@ __global__ void __launch_bounds__(32 * SOLVE_WARPS, 3) k_bwd_persist(SymDev S, S
   double* xr = smem + (size_t)warp * (A.max_m + 64 + 16 * 33);
   double* tv = xr + A.max_m;
   double* red = tv + 64;
+  int* ridx = reinterpret_cast<int*>(smem + (size_t)SOLVE_WARPS * (A.max_m + 64 + 16 * 33) + A.max_m + 128) +
+              warp * A.max_m;
   // CTA mode: top queue in reverse level order
   double* cx = smem + (size_t)SOLVE_WARPS * (A.max_m + 64 + 16 * 33);
   for (;;) {
@@ -733,7 +754,6 @@ __global__ void __launch_bounds__(32 * SOLVE_WARPS, 3) k_bwd_persist(SymDev S, S
     int* done = A.done_all + (int64_t)b * A.ns;
     if (!(A.skip && A.skip[b])) {
       bwd_cta_step(S, A, s, b, cx, cx + A.max_m, cx + A.max_m + 64, red, done);
-      fence_acq_rel();
     }
     __syncthreads();
     if (threadIdx.x == 0) st_release(done + s, A.epoch);
@@ -749,8 +769,7 @@ __global__ void __launch_bounds__(32 * SOLVE_WARPS, 3) k_bwd_persist(SymDev S, S
     for (int q = A.chunk_ptr[ch + 1] - 1; q >= A.chunk_ptr[ch]; --q) {
       const int s = A.queue[q];
       if (!sk) {
-        bwd_warp_step(S, A, s, b, lane, xr, tv, red, done);
-        fence_acq_rel();
+        bwd_warp_step(S, A, s, b, lane, xr, tv, red, ridx, done);
         __syncwarp();
       }
       if (lane == 0) st_release(done + s, A.epoch);
