@@ -490,6 +490,8 @@ struct ckkt_ctx {
   Sched Qfac{}, Qfwd{}, Qbwd{};
   int nchunk = 0, nq = 0, nsub = 0;
   int32_t *chunk_ptr = nullptr, *queue = nullptr, *sub_ptr = nullptr, *sub_nodes = nullptr, *topq = nullptr;
+  const SnMeta* qmeta = nullptr;  // metadata of the bottom queue, queue order
+  const SnMeta* tmeta = nullptr;  // metadata of the tiny subtrees' nodes, sub_nodes order
   int ntop = 0;
   int8_t* tinyflag = nullptr;
   std::vector<int8_t> tiny_host;
@@ -500,7 +502,7 @@ struct ckkt_ctx {
   std::vector<int> ev_phase;
   size_t ev_used = 0;
   int prof_phase = -1;
-  int64_t big_smem = 0, fac_smem = 0, sol_smem = 0;
+  int64_t big_smem = 0, fac_smem = 0, sol_smem = 0, fwd_smem = 0;
   int *notpd = nullptr, *minpiv = nullptr;
   // last refactor values (caller-owned, must stay valid until the next refactor)
   const double *w_val = nullptr, *g_val = nullptr, *h_val = nullptr, *sigma = nullptr, *d_s = nullptr,
@@ -674,18 +676,22 @@ ckkt_status setup_device(ckkt_ctx* c) {
     c->fac_smem = std::max<int64_t>(c->big_smem, 8 * SMALL_WARPS * SMALL_PANEL);
     c->sol_smem = 8 * ((int64_t)SOLVE_WARPS * (c->max_m + 64 + 16 * 33) + c->max_m + 128) +
                   4 * (int64_t)SOLVE_WARPS * c->max_m;  // + per-warp row indices (backward)
+    c->fwd_smem = 8 * ((int64_t)SOLVE_WARPS * (c->max_m + 64) + c->max_m + 64);
     if (c->fac_smem > 227 * 1024 || c->sol_smem > 227 * 1024) return CKKT_INVALID_ARG;
     CK(cudaFuncSetAttribute(k_factor_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->fac_smem));
-    CK(cudaFuncSetAttribute(k_fwd_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->sol_smem));
+    CK(cudaFuncSetAttribute(k_fwd_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->fwd_smem));
     CK(cudaFuncSetAttribute(k_bwd_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->sol_smem));
     int dev_sms = 0, occ = 0;
     CK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->opt.device));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_factor_persist, MF_THREADS, c->fac_smem));
     c->grid_fac = std::max(1, std::min(occ * dev_sms, c->ntask * B));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fwd_persist, 32 * SOLVE_WARPS, c->sol_smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fwd_persist, 32 * SOLVE_WARPS, c->fwd_smem));
     c->grid_fwd = std::max(1, std::min(occ * dev_sms, (A.ns * B + SOLVE_WARPS - 1) / SOLVE_WARPS));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bwd_persist, 32 * SOLVE_WARPS, c->sol_smem));
     c->grid_bwd = std::max(1, std::min(occ * dev_sms, (A.ns * B + SOLVE_WARPS - 1) / SOLVE_WARPS));
+    if (getenv("CKKT_VERBOSE"))
+      fprintf(stderr, "ckkt: grids factor %d fwd %d bwd %d, smem factor %lld fwd %lld bwd %lld, max_m %d\n", c->grid_fac,
+              c->grid_fwd, c->grid_bwd, (long long)c->fac_smem, (long long)c->fwd_smem, (long long)c->sol_smem, c->max_m);
     {  // tiny subtrees (one thread each) and the queue of the remaining supernodes (one warp each)
       const int ns = A.ns;
       const std::vector<int8_t>& T = c->tiny_host;
@@ -734,6 +740,15 @@ ckkt_status setup_device(ckkt_ctx* c) {
       c->nsub = (int)subs.size();
       c->sub_ptr = upload(sp, o, by);
       c->sub_nodes = upload(sn, o, by);
+      {
+        std::vector<SnMeta> tm(sn.size());
+        for (size_t k = 0; k < sn.size(); ++k) {
+          tm[k] = c->meta_h[sn[k]];
+          tm[k].pad1 = sn[k];
+        }
+        c->tmeta = upload(tm, o, by);
+        if (!c->tmeta && !sn.empty()) return CKKT_OUT_OF_MEMORY;
+      }
       c->tinyflag = upload(T, o, by);
       // top set: large supernodes (panel > TOP_PANEL doubles) and all their ancestors (one CTA each)
       std::vector<int8_t> top(ns, 0);
@@ -759,6 +774,16 @@ ckkt_status setup_device(ckkt_ctx* c) {
       c->ntop = (int)tq.size();
       c->queue = upload(q, o, by);
       c->topq = upload(tq, o, by);
+      {
+        std::vector<SnMeta> qm(q.size());
+        for (size_t k = 0; k < q.size(); ++k) {
+          qm[k] = c->meta_h[q[k]];
+          qm[k].pad0 = A.sparent[q[k]];
+          qm[k].pad1 = q[k];
+        }
+        c->qmeta = upload(qm, o, by);
+        if (!c->qmeta && !q.empty()) return CKKT_OUT_OF_MEMORY;
+      }
       const int64_t warps = (int64_t)c->grid_fwd * SOLVE_WARPS;
       std::vector<int32_t> cp{0};
       for (int l = 0; l < A.nlevels; ++l) {
@@ -1092,6 +1117,7 @@ namespace {
 SweepArgs sweep_args(ckkt_ctx* c, const Sched& Q, int epoch, double* x, const int* skip) {
   SweepArgs a;
   a.queue = c->queue;
+  a.qmeta = c->qmeta;
   a.chunk_ptr = c->chunk_ptr;
   a.nchunk = c->nchunk;
   a.top = c->topq;
@@ -1116,12 +1142,12 @@ void launch_fwd(ckkt_ctx* c, double* x, const int* skip) {
   cudaStream_t st = c->stream;
   prof_begin(c, 2);
   if (c->nsub > 0)
-    k_fwd_tiny<<<(c->nsub * c->B + 255) / 256, 256, 0, st>>>(c->S, c->sub_ptr, c->sub_nodes, c->nsub, c->B, c->L,
+    k_fwd_tiny<<<(c->nsub * c->B * TG + 255) / 256, 256, 0, st>>>(c->S, c->tmeta, c->sub_ptr, c->nsub, c->B, c->L,
                                                               c->Lsize, x, c->n, c->Vb, c->Vsize, skip);
   DBG_SYNC("k_fwd_tiny");
   ++c->epoch_fwd;
   if (c->nq + c->ntop > 0)
-    k_fwd_persist<<<c->grid_fwd, 32 * SOLVE_WARPS, c->sol_smem, st>>>(c->S, sweep_args(c, c->Qfwd, c->epoch_fwd, x, skip));
+    k_fwd_persist<<<c->grid_fwd, 32 * SOLVE_WARPS, c->fwd_smem, st>>>(c->S, sweep_args(c, c->Qfwd, c->epoch_fwd, x, skip));
   DBG_SYNC("k_fwd_persist");
   prof_end(c);
 }
@@ -1134,7 +1160,7 @@ void launch_bwd(ckkt_ctx* c, double* x, const int* skip) {
     k_bwd_persist<<<c->grid_bwd, 32 * SOLVE_WARPS, c->sol_smem, st>>>(c->S, sweep_args(c, c->Qbwd, c->epoch_bwd, x, skip));
   DBG_SYNC("k_bwd_persist");
   if (c->nsub > 0)
-    k_bwd_tiny<<<(c->nsub * c->B + 255) / 256, 256, 0, st>>>(c->S, c->sub_ptr, c->sub_nodes, c->nsub, c->B, c->L,
+    k_bwd_tiny<<<(c->nsub * c->B * TG + 255) / 256, 256, 0, st>>>(c->S, c->tmeta, c->sub_ptr, c->nsub, c->B, c->L,
                                                               c->Lsize, x, c->n, skip);
   DBG_SYNC("k_bwd_tiny");
   prof_end(c);

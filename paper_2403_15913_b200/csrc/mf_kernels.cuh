@@ -70,7 +70,11 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
   return v;
 }
 __device__ __forceinline__ void st_release(int* p, int v) {
+#ifdef CKKT_DEBUG_NO_RELEASE  // timing experiments only: drops the release ordering (results may be wrong)
+  asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+#else
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+#endif
 }
 __device__ int g_debug_nowait = 0;  // debug only: skip dependency waits (timing experiments)
 __device__ unsigned long long* g_debug_ts = nullptr;  // debug only: [ns][4] ticket/wake/end times of sweeps
@@ -518,6 +522,7 @@ __device__ __forceinline__ int warp_ticket(int* ctr_slot, int lane, volatile int
 // ---------------------------------------------------------------------------------------------
 struct SweepArgs {
   const int32_t* queue;      // bottom supernodes, level order
+  const SnMeta* qmeta;       // their metadata in queue order (pad0 = parent, pad1 = supernode)
   const int32_t* chunk_ptr;  // chunks of the bottom queue
   int nchunk;
   const int32_t* top;        // top supernodes, level order
@@ -543,16 +548,11 @@ __device__ __forceinline__ int cta_ticket(int* ctr_slot, volatile int* sh) {
   return *sh;
 }
 
-// forward step of supernode s by one warp (v, y: per-warp shared scratch)
-__device__ __forceinline__ void fwd_warp_step(const SymDev& S, const SweepArgs& A, int s, int b, int lane, double* v,
-                                              double* y, ChMeta* cmeta, int* done) {
-  const SnMeta M = S.meta[s];
-  double* x = A.X + (int64_t)b * A.n;
-  const int f = M.f, w = M.w, m = M.m, mu = m - w;
-  const double* P = A.L + b * A.Lsize + M.pofs;
-  if (lane == 0) prefetch_l2(P, 8ll * m * w);  // the panel streams into L2 while the children are gathered
-  const unsigned long long t0 = g_debug_ts ? gtimer() : 0ull;
-  for (int i = lane; i < m; i += 32) v[i] = (i < w) ? x[f + i] : 0.0;
+// v[rel_c] += u_c for the children c of M (extend-add of the update vectors), children in
+// a fixed order (deterministic; rows inside one child are distinct so lanes never collide)
+__device__ __forceinline__ void warp_gather_children(const SymDev& S, const SweepArgs& A, const SnMeta& M, int b,
+                                                     int lane, double* v, ChMeta* cmeta, int* done) {
+  const double* Vb = A.Vb + b * A.Vsize;
   for (int cb = M.ch0; cb < M.ch1; cb += 32) {
     const int nc = min(32, M.ch1 - cb);
     if (lane < nc) {
@@ -563,12 +563,26 @@ __device__ __forceinline__ void fwd_warp_step(const SymDev& S, const SweepArgs& 
     __syncwarp();
     for (int k = 0; k < nc; ++k) {
       const ChMeta cm = cmeta[k];
-      const double* uc = A.Vb + b * A.Vsize + cm.vofs;
+      const double* uc = Vb + cm.vofs;
       const int32_t* rel = S.relmap + cm.relofs;
       for (int i = lane; i < cm.mc; i += 32) v[__ldg(rel + i)] += __ldcg(uc + i);
       __syncwarp();
     }
   }
+}
+
+// forward step of supernode s by one warp (v, y: per-warp shared scratch)
+__device__ __forceinline__ void fwd_warp_step(const SymDev& S, const SweepArgs& A, const SnMeta& M, int s, int b,
+                                              int lane, double* v, double* y, ChMeta* cmeta, int* done) {
+  double* x = A.X + (int64_t)b * A.n;
+  const int f = M.f, w = M.w, m = M.m, mu = m - w;
+  const double* P = A.L + b * A.Lsize + M.pofs;
+#ifndef CKKT_CHUNK_PREFETCH
+  if (lane == 0) prefetch_l2(P, 8ll * m * w);  // the panel streams into L2 while the children are gathered
+#endif
+  const unsigned long long t0 = g_debug_ts ? gtimer() : 0ull;
+  for (int i = lane; i < m; i += 32) v[i] = (i < w) ? x[f + i] : 0.0;
+  warp_gather_children(S, A, M, b, lane, v, cmeta, done);
   warp_gemv(P, m, w, w, v, nullptr, 1.0, y, lane);  // y = Z v[0:w]  (Z strict upper part is zero)
   __syncwarp();
   for (int i = lane; i < w; i += 32) x[f + i] = y[i];
@@ -578,6 +592,24 @@ __device__ __forceinline__ void fwd_warp_step(const SymDev& S, const SweepArgs& 
     g_debug_ts[4 * s + 1] = t0;
     g_debug_ts[4 * s + 2] = gtimer();
     g_debug_ts[4 * s + 3] = 0;
+  }
+}
+
+// stage the metadata of queue entries [q0, q0 + n) (n <= 16) into shared memory and start the
+// L2 prefetch of their panels (and, backward, of their row index lists)
+__device__ __forceinline__ void warp_stage_chunk(const SymDev& S, const SweepArgs& A, int q0, int n, int b, int lane,
+                                                 SnMeta* msh, bool rows) {
+  const long long* src = reinterpret_cast<const long long*>(A.qmeta + q0);
+  long long* dst = reinterpret_cast<long long*>(msh);
+  constexpr int WPM = sizeof(SnMeta) / 8;
+  for (int k = lane; k < n * WPM; k += 32) dst[k] = __ldg(src + k);
+  __syncwarp();
+  if (lane < n) {
+    const SnMeta& M = msh[lane];
+#ifdef CKKT_CHUNK_PREFETCH
+    prefetch_l2(A.L + b * A.Lsize + M.pofs, 8ll * M.m * M.w);
+#endif
+    if (rows) prefetch_l2(S.srows + M.r0 + M.w, 4ll * (M.m - M.w));
   }
 }
 
@@ -625,6 +657,7 @@ __global__ void __launch_bounds__(32 * SOLVE_WARPS, SOLVE_MINB) k_fwd_persist(Sy
   extern __shared__ double smem[];
   __shared__ int tk_sh[SOLVE_WARPS + 1];
   __shared__ ChMeta cmeta_all[SOLVE_WARPS][32];
+  __shared__ SnMeta msh_all[SOLVE_WARPS][16];
   if (blockIdx.x == 0 && threadIdx.x == 0) {  // slots of the next launch
     A.ctr[(A.epoch + 1) & 1] = 0;
     A.ctr[2 + ((A.epoch + 1) & 1)] = 0;
@@ -633,6 +666,7 @@ __global__ void __launch_bounds__(32 * SOLVE_WARPS, SOLVE_MINB) k_fwd_persist(Sy
   double* v = smem + (size_t)warp * (A.max_m + 64);
   double* y = v + A.max_m;
   ChMeta* cmeta = cmeta_all[warp];
+  SnMeta* msh = msh_all[warp];
   // warp mode: bottom queue in chunks
   for (;;) {
     const int t = warp_ticket(&A.ctr[A.epoch & 1], lane, &tk_sh[warp]);
@@ -640,14 +674,17 @@ __global__ void __launch_bounds__(32 * SOLVE_WARPS, SOLVE_MINB) k_fwd_persist(Sy
     const int ch = t / A.B, b = t % A.B;
     int* done = A.done_all + (int64_t)b * A.ns;
     const bool sk = A.skip && A.skip[b];
-    for (int q = A.chunk_ptr[ch]; q < A.chunk_ptr[ch + 1]; ++q) {
-      const int s = A.queue[q];
+    const int q0 = A.chunk_ptr[ch], n = A.chunk_ptr[ch + 1] - q0;
+    if (!sk) warp_stage_chunk(S, A, q0, n, b, lane, msh, false);
+    for (int j = 0; j < n; ++j) {
+      const int s = sk ? A.queue[q0 + j] : msh[j].pad1;
       if (!sk) {
-        fwd_warp_step(S, A, s, b, lane, v, y, cmeta, done);
+        fwd_warp_step(S, A, msh[j], s, b, lane, v, y, cmeta, done);
         __syncwarp();
       }
       if (lane == 0) st_release(done + s, A.epoch);
     }
+    __syncwarp();
   }
   // CTA mode: top queue
   double* vc = smem + (size_t)SOLVE_WARPS * (A.max_m + 64);
@@ -665,14 +702,15 @@ __global__ void __launch_bounds__(32 * SOLVE_WARPS, SOLVE_MINB) k_fwd_persist(Sy
 }
 
 // backward step of supernode s by one warp: x_s = Z^T (y_s - L21^T x_R)
-__device__ __forceinline__ void bwd_warp_step(const SymDev& S, const SweepArgs& A, int s, int b, int lane, double* xr,
-                                              double* tv, double* red, int* ridx, int* done) {
-  const SnMeta M = S.meta[s];
-  const int p = S.sparent[s];
+__device__ __forceinline__ void bwd_warp_step(const SymDev& S, const SweepArgs& A, const SnMeta& M, int s, int b,
+                                              int lane, double* xr, double* tv, double* red, int* ridx, int* done) {
+  const int p = M.pad0;
   double* x = A.X + (int64_t)b * A.n;
   const int f = M.f, w = M.w, m = M.m, mu = m - w;
   const double* P = A.L + b * A.Lsize + M.pofs;
+#ifndef CKKT_CHUNK_PREFETCH
   if (lane == 0) prefetch_l2(P, 8ll * m * w);  // independent of the parent: overlap with the wait
+#endif
   for (int i = lane; i < w; i += 32) tv[i] = x[f + i];
   for (int i = lane; i < mu; i += 32) ridx[i] = __ldg(S.srows + M.r0 + w + i);
   const unsigned long long t0 = g_debug_ts ? gtimer() : 0ull;
@@ -735,6 +773,7 @@ __device__ __forceinline__ void bwd_cta_step(const SymDev& S, const SweepArgs& A
 __global__ void __launch_bounds__(32 * SOLVE_WARPS, SOLVE_MINB) k_bwd_persist(SymDev S, SweepArgs A) {
   extern __shared__ double smem[];
   __shared__ int tk_sh[SOLVE_WARPS + 1];
+  __shared__ SnMeta msh_all[SOLVE_WARPS][16];
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     A.ctr[(A.epoch + 1) & 1] = 0;
     A.ctr[2 + ((A.epoch + 1) & 1)] = 0;
@@ -766,14 +805,18 @@ __global__ void __launch_bounds__(32 * SOLVE_WARPS, SOLVE_MINB) k_bwd_persist(Sy
     const int ch = A.nchunk - 1 - t / A.B, b = t % A.B;
     int* done = A.done_all + (int64_t)b * A.ns;
     const bool sk = A.skip && A.skip[b];
-    for (int q = A.chunk_ptr[ch + 1] - 1; q >= A.chunk_ptr[ch]; --q) {
-      const int s = A.queue[q];
+    const int q0 = A.chunk_ptr[ch], n = A.chunk_ptr[ch + 1] - q0;
+    SnMeta* msh = msh_all[warp];
+    if (!sk) warp_stage_chunk(S, A, q0, n, b, lane, msh, true);
+    for (int j = n - 1; j >= 0; --j) {
+      const int s = sk ? A.queue[q0 + j] : msh[j].pad1;
       if (!sk) {
-        bwd_warp_step(S, A, s, b, lane, xr, tv, red, ridx, done);
+        bwd_warp_step(S, A, msh[j], s, b, lane, xr, tv, red, ridx, done);
         __syncwarp();
       }
       if (lane == 0) st_release(done + s, A.epoch);
     }
+    __syncwarp();
   }
 }
 
@@ -791,88 +834,128 @@ __global__ void __launch_bounds__(32 * SOLVE_WARPS, SOLVE_MINB) k_bwd_persist(Sy
 #endif
 constexpr int TINY_M = CKKT_TINY_M, TINY_W = CKKT_TINY_W;
 
+// Sweeps of the tiny subtrees: a group of TG = 8 lanes per (subtree, instance), lanes over the
+// (at most 32) rows of each node, so panel and update-vector accesses are coalesced inside a group;
+// nodes in postorder (forward) / reverse postorder (backward).  tmeta = SnMeta in sub_nodes order.
+#ifndef CKKT_TG
+#define CKKT_TG 8
+#endif
+constexpr int TG = CKKT_TG;
+static_assert(TINY_M <= 32 && 32 % TG == 0, "tiny sweep layout");
+
 __global__ void __launch_bounds__(256)
-    k_fwd_tiny(SymDev S, const int32_t* __restrict__ sub_ptr, const int32_t* __restrict__ sub_nodes, int nsub, int B,
+    k_fwd_tiny(SymDev S, const SnMeta* __restrict__ tmeta, const int32_t* __restrict__ sub_ptr, int nsub, int B,
                const double* __restrict__ L, int64_t Lsize, double* X, int n, double* Vb, int64_t Vsize,
                const int* __restrict__ skip) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nsub * B) return;
-  const int sub = t / B, b = t % B;
+  __shared__ double vsh_all[256 / TG][TINY_M];
+  const int gid = (blockIdx.x * blockDim.x + threadIdx.x) / TG, g = threadIdx.x % TG;
+  if (gid >= nsub * B) return;  // group-uniform
+  const unsigned mask = (TG == 32 ? 0xFFFFFFFFu : ((1u << TG) - 1u)) << ((threadIdx.x & 31) & ~(TG - 1));
+  const int sub = gid / B, b = gid % B;
   if (skip && skip[b]) return;
+  double* v = vsh_all[threadIdx.x / TG];
   double* x = X + (int64_t)b * n;
   double* Vbb = Vb + b * Vsize;
-  for (int q = sub_ptr[sub]; q < sub_ptr[sub + 1]; ++q) {
-    const int s = sub_nodes[q];
-    const int f = S.sfirst[s], w = S.sfirst[s + 1] - f;
-    const int m = (int)(S.srowptr[s + 1] - S.srowptr[s]);
-    const double* P = L + b * Lsize + S.pofs[s];
-    double v[TINY_M], y[TINY_W];
+  const int q1 = sub_ptr[sub + 1];
+  for (int q = sub_ptr[sub]; q < q1; ++q) {
+    const SnMeta M = tmeta[q];
+    const int f = M.f, w = M.w, m = M.m;
+    const double* P = L + b * Lsize + M.pofs;
 #pragma unroll
-    for (int i = 0; i < TINY_M; ++i) v[i] = 0.0;
-    for (int i = 0; i < w; ++i) v[i] = x[f + i];
-    for (int ci = S.ch_ptr[s]; ci < S.ch_ptr[s + 1]; ++ci) {
-      const int c = S.ch_list[ci];
-      const int mc = off_rows(S, c);
-      const double* uc = Vbb + S.vofs[c];
-      const int32_t* rel = S.relmap + S.relofs[c];
-      for (int i = 0; i < mc; ++i) v[rel[i]] += uc[i];
+    for (int i = g; i < TINY_M; i += TG) v[i] = (i < w) ? x[f + i] : 0.0;
+    __syncwarp(mask);
+    for (int ci = M.ch0; ci < M.ch1; ++ci) {
+      const ChMeta cm = S.chmeta[ci];
+      const double* uc = Vbb + cm.vofs;
+      const int32_t* rel = S.relmap + cm.relofs;
+      for (int i = g; i < cm.mc; i += TG) v[__ldg(rel + i)] += __ldcg(uc + i);
+      __syncwarp(mask);
     }
+    // y = Z v[0:w] (every lane of the group, broadcast loads); lane k < w stores y_k
+    double y[TINY_W];
 #pragma unroll
     for (int k = 0; k < TINY_W; ++k) {
       double acc = 0.0;
-      if (k < w)
-        for (int j = 0; j <= k; ++j) acc += P[k + j * m] * v[j];
+#pragma unroll
+      for (int j = 0; j < TINY_W; ++j)
+        if (j <= k && k < w) acc += P[k + j * m] * v[j];
       y[k] = acc;
     }
-    for (int k = 0; k < w; ++k) x[f + k] = y[k];
-    double* us = Vbb + S.vofs[s];
-    for (int i = w; i < m; ++i) {
-      double acc = v[i];
 #pragma unroll
-      for (int k = 0; k < TINY_W; ++k)
-        if (k < w) acc -= P[i + k * m] * y[k];
-      us[i - w] = acc;
+    for (int k = 0; k < TINY_W; ++k)
+      if (k % TG == g && k < w) x[f + k] = y[k];
+    double* us = Vbb + M.vofs;
+#pragma unroll
+    for (int i0 = 0; i0 < TINY_M; i0 += TG) {
+      const int i = i0 + g;
+      if (i >= w && i < m) {
+        double acc = v[i];
+#pragma unroll
+        for (int k = 0; k < TINY_W; ++k)
+          if (k < w) acc -= P[i + k * m] * y[k];
+        us[i - w] = acc;
+      }
     }
+    __syncwarp(mask);
   }
 }
 
 __global__ void __launch_bounds__(256)
-    k_bwd_tiny(SymDev S, const int32_t* __restrict__ sub_ptr, const int32_t* __restrict__ sub_nodes, int nsub, int B,
+    k_bwd_tiny(SymDev S, const SnMeta* __restrict__ tmeta, const int32_t* __restrict__ sub_ptr, int nsub, int B,
                const double* __restrict__ L, int64_t Lsize, double* X, int n, const int* __restrict__ skip) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nsub * B) return;
-  const int sub = t / B, b = t % B;
+  __shared__ double red_all[256 / TG][TINY_W][TG + 1];
+  const int gid = (blockIdx.x * blockDim.x + threadIdx.x) / TG, g = threadIdx.x % TG;
+  if (gid >= nsub * B) return;
+  const unsigned mask = (TG == 32 ? 0xFFFFFFFFu : ((1u << TG) - 1u)) << ((threadIdx.x & 31) & ~(TG - 1));
+  const int sub = gid / B, b = gid % B;
   if (skip && skip[b]) return;
+  auto red = red_all[threadIdx.x / TG];
   double* x = X + (int64_t)b * n;
-  for (int q = sub_ptr[sub + 1] - 1; q >= sub_ptr[sub]; --q) {
-    const int s = sub_nodes[q];
-    const int f = S.sfirst[s], w = S.sfirst[s + 1] - f;
-    const int64_t r0 = S.srowptr[s];
-    const int m = (int)(S.srowptr[s + 1] - r0);
-    const double* P = L + b * Lsize + S.pofs[s];
-    double tv[TINY_W];
+  const int q0 = sub_ptr[sub];
+  for (int q = sub_ptr[sub + 1] - 1; q >= q0; --q) {
+    const SnMeta M = tmeta[q];
+    const int f = M.f, w = M.w, m = M.m;
+    const double* P = L + b * Lsize + M.pofs;
+    // partial t_c = -sum_{rows i of this lane} L21[i, c] x_R[i]
+    double part[TINY_W];
 #pragma unroll
-    for (int c = 0; c < TINY_W; ++c) tv[c] = (c < w) ? x[f + c] : 0.0;
-    for (int i = w; i < m; ++i) {
-      const double xi = x[S.srows[r0 + i]];
+    for (int c = 0; c < TINY_W; ++c) part[c] = 0.0;
 #pragma unroll
-      for (int c = 0; c < TINY_W; ++c)
-        if (c < w) tv[c] -= P[i + c * m] * xi;
+    for (int i0 = 0; i0 < TINY_M; i0 += TG) {
+      const int i = i0 + g;
+      if (i >= w && i < m) {
+        const double xi = __ldcg(x + __ldg(S.srows + M.r0 + i));
+#pragma unroll
+        for (int c = 0; c < TINY_W; ++c)
+          if (c < w) part[c] -= P[i + c * m] * xi;
+      }
     }
 #pragma unroll
+    for (int c = 0; c < TINY_W; ++c) red[c][g] = part[c];
+    __syncwarp(mask);
+    double tv[TINY_W];
+#pragma unroll
+    for (int c = 0; c < TINY_W; ++c) {
+      double acc = (c < w) ? x[f + c] : 0.0;
+#pragma unroll
+      for (int l = 0; l < TG; ++l) acc += red[c][l];
+      tv[c] = acc;
+    }
+    // x_s = Z^T t: lane i < w computes row i
+#pragma unroll
     for (int i = 0; i < TINY_W; ++i) {
-      if (i < w) {
+      if (i % TG == g && i < w) {
         double acc = 0.0;
-        for (int k = i; k < w; ++k) acc += P[k + i * m] * tv[k];
+#pragma unroll
+        for (int k = 0; k < TINY_W; ++k)
+          if (k >= i && k < w) acc += P[k + i * m] * tv[k];
         x[f + i] = acc;
       }
     }
+    __syncwarp(mask);
   }
 }
 
-// Factor of tiny subtrees: one thread per subtree, nodes in postorder.  The front panel lives in
-// thread-local memory; the update matrices go to Ub and are consumed by the same thread (children)
-// or by the persistent kernel (subtree root) launched afterwards.
 __global__ void __launch_bounds__(128)
     k_factor_tiny(SymDev S, const int32_t* __restrict__ sub_ptr, const int32_t* __restrict__ sub_nodes, int nsub,
                   int B, double* L, int64_t Lsize, double* Ub, int64_t Usize, const double* __restrict__ Kval,

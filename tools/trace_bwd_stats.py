@@ -38,3 +38,13 @@ for k in [0, 1]:
         print(f"mode {'warp' if k == 0 else 'cta'}: n={ss.sum()} wake range [{wake[ss].min():.0f},{wake[ss].max():.0f}] end max {end[ss].max():.0f} proc sum {proc[ss].sum():.0f} us")
 hist, edges = np.histogram(end[done], bins=10)
 print('completions per time bin:', list(zip(np.round(edges[:-1]).astype(int), hist)))
+chp = get(ctx, 9, np.int32); chl = get(ctx, 10, np.int32)
+h = np.zeros(len(w), np.int32)
+for s in range(len(w)):  # children precede parents (postorder)
+    c = chl[chp[s]:chp[s + 1]]
+    if len(c): h[s] = h[c].max() + 1
+print('height: count traced, tick min, wake min/max, end max, proc mean, bytes MB')
+for lv in range(h.max() + 1):
+    ss = done & (h == lv)
+    if ss.any():
+        print(f"  h={lv:2d} n={ss.sum():7d} tick [{tick[ss].min():6.0f}] wake [{wake[ss].min():6.0f},{wake[ss].max():6.0f}] end {end[ss].max():6.0f} proc {proc[ss].mean():5.1f} MB {pw[ss].sum()*8/1e6:7.1f}")
