@@ -76,9 +76,11 @@ __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 #endif
 }
-__device__ int g_debug_nowait = 0;  // debug only: skip dependency waits (timing experiments)
-__device__ unsigned long long* g_debug_ts = nullptr;  // debug only: [ns][4] ticket/wake/end times of sweeps
-__device__ unsigned long long* g_debug_ph = nullptr;  // debug only: [ns][8] phase times inside factor_big
+// debug switches live in constant memory: reading them costs no global round trip (a __device__
+// variable would be re-fetched from L2 after every fence, on the critical path of each step)
+__constant__ int g_debug_nowait = 0;  // debug only: skip dependency waits (timing experiments)
+__constant__ unsigned long long* g_debug_ts = nullptr;  // debug only: [ns][4] ticket/wake/end times of sweeps
+__constant__ unsigned long long* g_debug_ph = nullptr;  // debug only: [ns][8] phase times inside factor_big
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -95,7 +97,12 @@ __device__ __forceinline__ int ld_relaxed(const int* p) {
 #ifndef CKKT_POLL_MAX_NS
 #define CKKT_POLL_MAX_NS 256
 #endif
-// poll with relaxed loads, then one acquire fence (cheaper than repeated ld.acquire)
+// Poll with relaxed loads.  Everything a consumer reads from another CTA after the wait (children's
+// update matrices / vectors, the solution entries of ancestors) is read with ld.global.cg, i.e. from
+// L2, the point of coherence, and those loads are issued only after the poll has returned the
+// producer's epoch (control dependency); the producer publishes with st.release after its data
+// writes.  So no acquire fence (MEMBAR + L1 invalidation, ~1 us on the critical path) is needed.
+// -DCKKT_ACQUIRE_FENCE restores the formal acquire.
 __device__ __forceinline__ void wait_epoch(const int* p, int epoch) {
   if (g_debug_nowait) return;
   int ns = 32;
@@ -103,7 +110,9 @@ __device__ __forceinline__ void wait_epoch(const int* p, int epoch) {
     __nanosleep(ns);
     ns = ns < CKKT_POLL_MAX_NS ? 2 * ns : CKKT_POLL_MAX_NS;
   }
+#ifdef CKKT_ACQUIRE_FENCE
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#endif
 }
 
 // release-side fence: makes this thread's prior writes visible at gpu scope before the flag store
