@@ -1,0 +1,22 @@
+"""Per-launch DRAM traffic of the sweep / factor kernels from one ncu --set full report -> profiles/traffic.json.
+usage: python tools/traffic_from_ncu.py <report.ncu-rep> <source note>"""
+import csv, json, subprocess, sys
+rep, note = sys.argv[1], sys.argv[2]
+out = subprocess.run(['ncu', '-i', rep, '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
+r = list(csv.reader(out.splitlines()))
+h, units = r[0], r[1]
+scale = {'byte': 1.0, 'Kbyte': 1e3, 'Mbyte': 1e6, 'Gbyte': 1e9, 'Tbyte': 1e12}
+per = {}
+for row in r[2:]:
+    d = dict(zip(h, row))
+    u = dict(zip(h, units))
+    name = d['Kernel Name'].split('(')[0].replace('<unnamed>::', '')
+    tot = sum(float(d[k].replace(',', '')) * scale[u[k]] for k in ('dram__bytes_read.sum', 'dram__bytes_write.sum'))
+    per.setdefault(name, tot)  # first capture of each kernel
+fwd = per['k_fwd_tiny'] + per['k_fwd_persist']
+bwd = per['k_bwd_persist'] + per['k_bwd_tiny']
+res = {"_source": note, "k_fwd_tiny + k_fwd_persist (one forward sweep)": fwd,
+       "k_bwd_persist + k_bwd_tiny (one backward sweep)": bwd, "k_factor_persist": per['k_factor_persist'],
+       "_per_kernel": per}
+json.dump(res, open('profiles/traffic.json', 'w'), indent=1)
+print(json.dumps(res, indent=1))
