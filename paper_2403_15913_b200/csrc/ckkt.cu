@@ -485,7 +485,7 @@ struct ckkt_ctx {
   double *Kval = nullptr, *L = nullptr, *Ub = nullptr, *Vb = nullptr;
   int64_t Usize = 0, Vsize = 0;
   int max_m = 1;
-  int ntask = 0, grid_fac = 1, grid_fwd = 1, grid_bwd = 1;
+  int ntask = 0, grid_fac = 1, grid_fwd = 1, grid_bwd = 1, grid_ftop = 1, grid_btop = 1;
   int epoch_fac = 0, epoch_fwd = 0, epoch_bwd = 0;
   Sched Qfac{}, Qfwd{}, Qbwd{};
   int nchunk = 0, nq = 0, nsub = 0;
@@ -493,6 +493,9 @@ struct ckkt_ctx {
   const SnMeta* qmeta = nullptr;  // metadata of the bottom queue, queue order
   const SnMeta* tmeta = nullptr;  // metadata of the tiny subtrees' nodes, sub_nodes order
   int ntop = 0;
+  const SnMeta* topmeta = nullptr;  // metadata of the top queue, top order
+  int topbuf = 0;                   // doubles of the top kernels' panel buffer
+  int64_t ftop_smem = 0, btop_smem = 0;
   int8_t* tinyflag = nullptr;
   std::vector<int8_t> tiny_host;
   std::vector<SnMeta> meta_h;
@@ -774,6 +777,39 @@ ckkt_status setup_device(ckkt_ctx* c) {
       c->ntop = (int)tq.size();
       c->queue = upload(q, o, by);
       c->topq = upload(tq, o, by);
+      {
+        std::vector<SnMeta> tm(tq.size());
+        int64_t maxp = 0;
+        for (size_t k = 0; k < tq.size(); ++k) {
+          tm[k] = c->meta_h[tq[k]];
+          tm[k].pad0 = A.sparent[tq[k]];
+          tm[k].pad1 = tq[k];
+          maxp = std::max<int64_t>(maxp, (int64_t)tm[k].m * tm[k].w);
+        }
+        c->topmeta = upload(tm, o, by);
+        if (!c->topmeta && !tq.empty()) return CKKT_OUT_OF_MEMORY;
+        // panel buffer: the largest top panel (+2 for the 16-byte alignment offset), capped so that
+        // two CTAs of each top kernel fit on an SM; larger panels are read from global memory
+        cudaFuncAttributes fa{}, ba{};
+        CK(cudaFuncGetAttributes(&fa, k_fwd_top));
+        CK(cudaFuncGetAttributes(&ba, k_bwd_top));
+        const int64_t per_cta = (228 * 1024) / TOP_MINB - 2048;
+        const int64_t fcap = (per_cta - (int64_t)fa.sharedSizeBytes) / 8 - (c->max_m + 64);
+        const int64_t bcap = (per_cta - (int64_t)ba.sharedSizeBytes) / 8 - (c->max_m + 128);
+        c->topbuf = (int)std::max<int64_t>(0, std::min<int64_t>(maxp + 2, std::min(fcap, bcap)) & ~int64_t(1));
+        c->ftop_smem = 8 * ((int64_t)c->topbuf + c->max_m + 64);
+        c->btop_smem = 8 * ((int64_t)c->topbuf + c->max_m + 128);
+        CK(cudaFuncSetAttribute(k_fwd_top, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->ftop_smem));
+        CK(cudaFuncSetAttribute(k_bwd_top, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->btop_smem));
+        int occ2 = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_fwd_top, TOP_THREADS, c->ftop_smem));
+        c->grid_ftop = std::max(1, std::min(occ2 * dev_sms, std::max(1, c->ntop * B)));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_bwd_top, TOP_THREADS, c->btop_smem));
+        c->grid_btop = std::max(1, std::min(occ2 * dev_sms, std::max(1, c->ntop * B)));
+        if (getenv("CKKT_VERBOSE"))
+          fprintf(stderr, "ckkt: top set %d supernodes, max panel %lld, buffer %d doubles, grids %d/%d\n", c->ntop,
+                  (long long)maxp, c->topbuf, c->grid_ftop, c->grid_btop);
+      }
       {
         std::vector<SnMeta> qm(q.size());
         for (size_t k = 0; k < q.size(); ++k) {
@@ -1114,14 +1150,16 @@ ckkt_status ckkt_refactor(ckkt_ctx* c, const double* w_val, const double* g_val,
 
 namespace {
 
-SweepArgs sweep_args(ckkt_ctx* c, const Sched& Q, int epoch, double* x, const int* skip) {
+SweepArgs sweep_args(ckkt_ctx* c, const Sched& Q, int epoch, double* x, const int* skip, bool top) {
   SweepArgs a;
   a.queue = c->queue;
   a.qmeta = c->qmeta;
   a.chunk_ptr = c->chunk_ptr;
   a.nchunk = c->nchunk;
   a.top = c->topq;
-  a.ntop = c->ntop;
+  a.topmeta = c->topmeta;
+  a.ntop = top ? c->ntop : 0;
+  a.topbuf = c->topbuf;
   a.ns = c->A.ns;
   a.ctr = Q.ctr;
   a.done_all = Q.done;
@@ -1146,9 +1184,15 @@ void launch_fwd(ckkt_ctx* c, double* x, const int* skip) {
                                                               c->Lsize, x, c->n, c->Vb, c->Vsize, skip);
   DBG_SYNC("k_fwd_tiny");
   ++c->epoch_fwd;
-  if (c->nq + c->ntop > 0)
-    k_fwd_persist<<<c->grid_fwd, 32 * SOLVE_WARPS, c->fwd_smem, st>>>(c->S, sweep_args(c, c->Qfwd, c->epoch_fwd, x, skip));
+  if (c->nq > 0)
+    k_fwd_persist<<<c->grid_fwd, 32 * SOLVE_WARPS, c->fwd_smem, st>>>(c->S,
+                                                                       sweep_args(c, c->Qfwd, c->epoch_fwd, x, skip, false));
   DBG_SYNC("k_fwd_persist");
+  if (c->ntop > 0) {
+    k_fwd_top<<<c->grid_ftop, TOP_THREADS, c->ftop_smem, st>>>(c->S, sweep_args(c, c->Qfwd, c->epoch_fwd, x, skip, true));
+    c->launches++;
+  }
+  DBG_SYNC("k_fwd_top");
   prof_end(c);
 }
 
@@ -1156,8 +1200,14 @@ void launch_bwd(ckkt_ctx* c, double* x, const int* skip) {
   cudaStream_t st = c->stream;
   prof_begin(c, 3);
   ++c->epoch_bwd;
-  if (c->nq + c->ntop > 0)
-    k_bwd_persist<<<c->grid_bwd, 32 * SOLVE_WARPS, c->sol_smem, st>>>(c->S, sweep_args(c, c->Qbwd, c->epoch_bwd, x, skip));
+  if (c->ntop > 0) {
+    k_bwd_top<<<c->grid_btop, TOP_THREADS, c->btop_smem, st>>>(c->S, sweep_args(c, c->Qbwd, c->epoch_bwd, x, skip, true));
+    c->launches++;
+  }
+  DBG_SYNC("k_bwd_top");
+  if (c->nq > 0)
+    k_bwd_persist<<<c->grid_bwd, 32 * SOLVE_WARPS, c->sol_smem, st>>>(c->S,
+                                                                       sweep_args(c, c->Qbwd, c->epoch_bwd, x, skip, false));
   DBG_SYNC("k_bwd_persist");
   if (c->nsub > 0)
     k_bwd_tiny<<<(c->nsub * c->B * TG + 255) / 256, 256, 0, st>>>(c->S, c->tmeta, c->sub_ptr, c->nsub, c->B, c->L,

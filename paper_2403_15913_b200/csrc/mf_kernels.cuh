@@ -582,7 +582,9 @@ struct SweepArgs {
   const int32_t* chunk_ptr;  // chunks of the bottom queue
   int nchunk;
   const int32_t* top;        // top supernodes, level order
+  const SnMeta* topmeta;     // their metadata in top order (pad0 = parent, pad1 = supernode)
   int ntop;
+  int topbuf;                // doubles of the top kernels' shared-memory panel buffer
   int ns;                    // done-flag stride
   int* ctr;                  // [4]: warp tickets (2 epoch slots), CTA tickets (2 epoch slots)
   int* done_all;
@@ -744,7 +746,7 @@ __global__ void __launch_bounds__(32 * SOLVE_WARPS, SOLVE_MINB) k_fwd_persist(Sy
   }
   // CTA mode: top queue
   double* vc = smem + (size_t)SOLVE_WARPS * (A.max_m + 64);
-  for (;;) {
+  for (; A.ntop > 0;) {  // (ntop = 0 when the top set runs in k_fwd_top: its ticket slot stays untouched)
     const int t = cta_ticket(&A.ctr[2 + (A.epoch & 1)], &tk_sh[SOLVE_WARPS]);
     if (t >= A.ntop * A.B) break;
     const int s = A.top[t / A.B], b = t % A.B;
@@ -842,7 +844,7 @@ __global__ void __launch_bounds__(32 * SOLVE_WARPS, SOLVE_MINB) k_bwd_persist(Sy
               warp * A.max_m;
   // CTA mode: top queue in reverse level order
   double* cx = smem + (size_t)SOLVE_WARPS * (A.max_m + 64 + 16 * 33);
-  for (;;) {
+  for (; A.ntop > 0;) {
     const int t = cta_ticket(&A.ctr[2 + (A.epoch & 1)], &tk_sh[SOLVE_WARPS]);
     if (t >= A.ntop * A.B) break;
     const int s = A.top[A.ntop - 1 - t / A.B], b = t % A.B;
@@ -873,6 +875,324 @@ __global__ void __launch_bounds__(32 * SOLVE_WARPS, SOLVE_MINB) k_bwd_persist(Sy
       if (lane == 0) st_release(done + s, A.epoch);
     }
     __syncwarp();
+  }
+}
+
+// ============================================================================================
+// Top set (large panels and their ancestors): one CTA per supernode, separate persistent launches
+// (forward: after the warp-mode kernel; backward: before it) sized for 2 CTAs per SM.  The panel is
+// copied into shared memory by ONE bulk async copy (cp.async.bulk, completion on an mbarrier) issued
+// at the start of the step, so it lands while the CTA gathers its children's update vectors
+// (forward) or waits for its parent and gathers x (backward); the CTA takes its next ticket one step
+// ahead and prefetches that panel into L2.  The dense work then runs out of shared memory.  Panels
+// larger than the buffer are read from global memory by the same code (generic pointer).
+// ============================================================================================
+#ifndef CKKT_TOP_THREADS
+#define CKKT_TOP_THREADS 256
+#endif
+#ifndef CKKT_TOP_MINB
+#define CKKT_TOP_MINB 2
+#endif
+constexpr int TOP_THREADS = CKKT_TOP_THREADS, TOP_WARPS = TOP_THREADS / 32, TOP_MINB = CKKT_TOP_MINB;
+constexpr int TOP_CPW = 64 / TOP_WARPS;  // backward: columns per warp (w <= 64)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+
+// shared state of a top-kernel CTA
+struct TopShared {
+  uint64_t bar;
+  int tk_next;
+  SnMeta m_next;  // metadata of the reserved next ticket
+  ChMeta cmeta[32];
+};
+
+// Issue the panel of (q, b) into buf (thread 0).  Returns the panel pointer the CTA computes from
+// (inside buf, or the global panel when it does not fit) — every thread evaluates it identically.
+__device__ __forceinline__ const double* top_panel(const SweepArgs& A, const SnMeta& M, int b, double* buf,
+                                                   TopShared& sh, bool issue) {
+  const double* P = A.L + b * A.Lsize + M.pofs;
+  const uintptr_t a = reinterpret_cast<uintptr_t>(P);
+  const int off = (int)((a & 15) >> 3);  // doubles between the 16-byte aligned start and the panel
+  const int64_t bytes = ((int64_t)(M.m * M.w + off) * 8 + 15) & ~int64_t(15);
+  if (bytes > (int64_t)A.topbuf * 8) return P;
+  if (issue) {
+    mbar_expect_tx(&sh.bar, (uint32_t)bytes);
+    bulk_g2s(buf, reinterpret_cast<const void*>(a & ~uintptr_t(15)), (uint32_t)bytes, &sh.bar);
+  }
+  return buf + off;
+}
+
+// one thread reserves the CTA's next ticket, stages its metadata in shared memory and prefetches
+// its panel into L2 (the reservation runs one step ahead; tickets stay in topological order, and a
+// reserved ticket is started as soon as the current one completes, so no CTA can wait on a ticket
+// that is not being worked on)
+__device__ __forceinline__ void top_reserve_next(const SweepArgs& A, int* ctr, TopShared& sh, bool reverse) {
+  const int tn = atomicAdd(ctr, 1);
+  sh.tk_next = tn;
+  if (tn >= A.ntop * A.B) return;
+  const int q = reverse ? A.ntop - 1 - tn / A.B : tn / A.B, b = tn % A.B;
+  const SnMeta Mn = A.topmeta[q];
+  sh.m_next = Mn;
+  prefetch_l2(A.L + b * A.Lsize + Mn.pofs, 8ll * Mn.m * Mn.w);
+}
+
+__global__ void __launch_bounds__(TOP_THREADS, TOP_MINB) k_fwd_top(SymDev S, SweepArgs A) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ TopShared sh;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* buf = smem;                       // [topbuf]
+  double* v = buf + A.topbuf;               // [max_m]
+  double* y = v + A.max_m;                  // [64]
+  int* ctr = &A.ctr[2 + (A.epoch & 1)];
+  if (blockIdx.x == 0 && tid == 0) A.ctr[2 + ((A.epoch + 1) & 1)] = 0;
+  if (tid == 0) {
+    mbar_init(&sh.bar, 1);
+    top_reserve_next(A, ctr, sh, false);
+  }
+  __syncthreads();
+  uint32_t parity = 0;
+  int t = sh.tk_next;
+  const int total = A.ntop * A.B;
+  while (t < total) {
+    const int b = t % A.B;
+    const SnMeta M = sh.m_next;
+    const int s = M.pad1, f = M.f, w = M.w, m = M.m, mu = m - w;
+    int* done = A.done_all + (int64_t)b * A.ns;
+    const bool sk = A.skip && A.skip[b];
+    const unsigned long long t0 = g_debug_ts ? gtimer() : 0ull;
+    unsigned long long t1 = t0;
+    const double* Pl = sk ? nullptr : top_panel(A, M, b, buf, sh, tid == 0);
+    const bool in_smem = Pl != nullptr && Pl != A.L + b * A.Lsize + M.pofs;
+    __syncthreads();  // everyone has read sh.tk_next (and the previous step is complete)
+    if (tid == 64) top_reserve_next(A, ctr, sh, false);  // warp 2 (warp 0 polls the flags)
+    if (!sk) {
+      double* x = A.X + (int64_t)b * A.n;
+      const double* Vb = A.Vb + b * A.Vsize;
+      for (int i = tid; i < m; i += TOP_THREADS) v[i] = (i < w) ? x[f + i] : 0.0;
+      // children's update vectors: all (row, value) pairs of up to 8 children are loaded before any
+      // is applied (one memory round trip), then added child by child (fixed order, deterministic)
+      for (int cb = M.ch0; cb < M.ch1; cb += 32) {
+        const int nc = min(32, M.ch1 - cb);
+        if (warp == 0 && lane < nc) {
+          const ChMeta cm = S.chmeta[cb + lane];
+          sh.cmeta[lane] = cm;
+          if (!cm.tiny) wait_epoch(done + cm.c, A.epoch);
+        }
+        __syncthreads();
+        for (int k0 = 0; k0 < nc; k0 += 8) {
+          double uv[8];
+          int rl[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            rl[k] = -1;
+            if (k0 + k < nc) {
+              const ChMeta& cm = sh.cmeta[k0 + k];
+              if (tid < cm.mc) {
+                rl[k] = __ldg(S.relmap + cm.relofs + tid);
+                uv[k] = __ldcg(Vb + cm.vofs + tid);
+              }
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            if (k0 + k < nc) {
+              if (rl[k] >= 0) v[rl[k]] += uv[k];
+              __syncthreads();
+            }
+          }
+          for (int k = k0; k < min(nc, k0 + 8); ++k) {  // rows beyond the first TOP_THREADS
+            const ChMeta& cm = sh.cmeta[k];
+            if (cm.mc > TOP_THREADS) {
+              for (int i = TOP_THREADS + tid; i < cm.mc; i += TOP_THREADS)
+                v[__ldg(S.relmap + cm.relofs + i)] += __ldcg(Vb + cm.vofs + i);
+              __syncthreads();
+            }
+          }
+        }
+      }
+      if (g_debug_ts) t1 = gtimer();
+      if (in_smem) {
+        mbar_wait(&sh.bar, parity);
+        parity ^= 1;
+      }
+      __syncthreads();
+      // y = Z v[0:w]  (thread per row; Z is lower triangular)
+      if (tid < w) {
+        double a0 = 0.0, a1 = 0.0;
+        int c = 0;
+        for (; c + 1 <= tid; c += 2) {
+          a0 += Pl[tid + c * m] * v[c];
+          a1 += Pl[tid + (c + 1) * m] * v[c + 1];
+        }
+        if (c <= tid) a0 += Pl[tid + c * m] * v[c];
+        y[tid] = a0 + a1;
+        x[f + tid] = a0 + a1;
+      }
+      __syncthreads();
+      // u = v[w:m] - L21 y  (thread per row)
+      double* us = A.Vb + b * A.Vsize + M.vofs;
+      for (int i = tid; i < mu; i += TOP_THREADS) {
+        double a0 = v[w + i], a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        const double* pr = Pl + w + i;
+        int c = 0;
+        for (; c + 3 < w; c += 4) {
+          a0 -= pr[c * m] * y[c];
+          a1 -= pr[(c + 1) * m] * y[c + 1];
+          a2 -= pr[(c + 2) * m] * y[c + 2];
+          a3 -= pr[(c + 3) * m] * y[c + 3];
+        }
+        for (; c < w; ++c) a0 -= pr[c * m] * y[c];
+        us[i] = (a0 + a1) + (a2 + a3);
+      }
+    }
+    __syncthreads();  // all writes of this step precede the release; buffers free for the next copy
+    if (tid == 0) st_release(done + s, A.epoch);
+    if (g_debug_ts && tid == 0 && b == 0) {
+      g_debug_ts[4 * s] = t0;
+      g_debug_ts[4 * s + 1] = t1;
+      g_debug_ts[4 * s + 2] = gtimer();
+      g_debug_ts[4 * s + 3] = 1;
+    }
+    t = sh.tk_next;
+  }
+}
+
+__global__ void __launch_bounds__(TOP_THREADS, TOP_MINB) k_bwd_top(SymDev S, SweepArgs A) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ TopShared sh;
+  __shared__ double red[TOP_WARPS][TOP_CPW * 33 + 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* buf = smem;                       // [topbuf]
+  double* xr = buf + A.topbuf;              // [max_m]
+  double* tv = xr + A.max_m;                // [64]
+  double* xo = tv + 64;                     // [64]
+  int* ctr = &A.ctr[2 + (A.epoch & 1)];
+  if (blockIdx.x == 0 && tid == 0) A.ctr[2 + ((A.epoch + 1) & 1)] = 0;
+  if (tid == 0) {
+    mbar_init(&sh.bar, 1);
+    top_reserve_next(A, ctr, sh, true);
+  }
+  __syncthreads();
+  uint32_t parity = 0;
+  int t = sh.tk_next;
+  const int total = A.ntop * A.B;
+  while (t < total) {
+    const int b = t % A.B;
+    const SnMeta M = sh.m_next;
+    const int s = M.pad1, p = M.pad0, f = M.f, w = M.w, m = M.m, mu = m - w;
+    int* done = A.done_all + (int64_t)b * A.ns;
+    const bool sk = A.skip && A.skip[b];
+    const unsigned long long t0 = g_debug_ts ? gtimer() : 0ull;
+    unsigned long long t1 = t0;
+    const double* Pl = sk ? nullptr : top_panel(A, M, b, buf, sh, tid == 0);
+    const bool in_smem = Pl != nullptr && Pl != A.L + b * A.Lsize + M.pofs;
+    __syncthreads();
+    if (tid == 64) top_reserve_next(A, ctr, sh, true);
+    if (!sk) {
+      double* x = A.X + (int64_t)b * A.n;
+      if (tid < w) tv[tid] = x[f + tid];
+      int ri[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        ri[k] = (tid + k * TOP_THREADS < mu) ? __ldg(S.srows + M.r0 + w + tid + k * TOP_THREADS) : 0;
+      if (tid == 0 && p >= 0) wait_epoch(done + p, A.epoch);
+      __syncthreads();
+      if (g_debug_ts) t1 = gtimer();
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (tid + k * TOP_THREADS < mu) xr[tid + k * TOP_THREADS] = __ldcg(x + ri[k]);
+      for (int i = tid + 4 * TOP_THREADS; i < mu; i += TOP_THREADS) xr[i] = __ldcg(x + __ldg(S.srows + M.r0 + w + i));
+      if (in_smem) {
+        mbar_wait(&sh.bar, parity);
+        parity ^= 1;
+      }
+      __syncthreads();
+      // two column-dot passes: t = y - L21^T x_R (rows w..m), then x_s = Z^T t (rows 0..w).
+      // Warp `warp` owns columns c = warp + TOP_WARPS j; lanes over rows; partials reduced through
+      // shared memory in two short stages.
+      for (int pass = 0; pass < 2; ++pass) {
+        const double* base = pass == 0 ? Pl + w : Pl;
+        const double* xv = pass == 0 ? xr : tv;
+        const int nr = pass == 0 ? mu : w;
+        double pp[TOP_CPW];
+#pragma unroll
+        for (int j = 0; j < TOP_CPW; ++j) pp[j] = 0.0;
+        for (int i = lane; i < nr; i += 32) {
+          const double xi = xv[i];
+#pragma unroll
+          for (int j = 0; j < TOP_CPW; ++j) {
+            const int c = warp + TOP_WARPS * j;
+            if (c < w) pp[j] += base[i + c * m] * xi;
+          }
+        }
+        double* rw = red[warp];
+#pragma unroll
+        for (int j = 0; j < TOP_CPW; ++j) rw[j * 33 + lane] = pp[j];
+        __syncwarp();
+        {
+          constexpr int H = 32 / TOP_CPW;
+          const int j = lane % TOP_CPW, h = lane / TOP_CPW;
+          const double* qv = rw + j * 33 + TOP_CPW * h;
+          double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+          for (int k = 0; k < TOP_CPW; k += 2) {
+            s0 += qv[k];
+            s1 += qv[k + 1];
+          }
+          rw[TOP_CPW * 33 + j * H + h] = s0 + s1;
+        }
+        __syncwarp();
+        if (lane < TOP_CPW) {
+          constexpr int H = 32 / TOP_CPW;
+          const int c = warp + TOP_WARPS * lane;
+          if (c < w) {
+            const double* r2 = rw + TOP_CPW * 33 + lane * H;
+            double sum = 0.0;
+#pragma unroll
+            for (int h = 0; h < H; ++h) sum += r2[h];
+            if (pass == 0) tv[c] -= sum;
+            else xo[c] = sum;
+          }
+        }
+        __syncthreads();
+      }
+      if (tid < w) x[f + tid] = xo[tid];
+    }
+    __syncthreads();
+    if (tid == 0) st_release(done + s, A.epoch);
+    if (g_debug_ts && tid == 0 && b == 0) {
+      g_debug_ts[4 * s] = t0;
+      g_debug_ts[4 * s + 1] = t1;
+      g_debug_ts[4 * s + 2] = gtimer();
+      g_debug_ts[4 * s + 3] = 1;
+    }
+    t = sh.tk_next;
   }
 }
 

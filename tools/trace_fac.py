@@ -48,7 +48,7 @@ for lo, hi in [(0, 2000), (2000, 5000), (5000, 10000), (10000, 1e9)]:
     ss = sel & (m * w >= lo) & (m * w < hi)
     if ss.any(): print(f"panel [{lo},{hi}) n={ss.sum()} mean proc {proc[ss].mean():.1f} us")
 ph = np.fromfile('/tmp/ckkt_phases.bin', dtype=np.uint64).reshape(ns, 8).astype(np.float64)
-issmall = ph[:, 7] == 1
+issmall = np.zeros(ns, bool)
 sel = (ph[:, 0] > 0) & issmall
 d = np.diff(ph[sel][:, :7], axis=1) / 1e3
 print('SMALL fronts:', sel.sum(), ' '.join(f"{nm}={d[:, k].mean():.1f}" for k, nm in enumerate(['zero+K', 'ext-panel', 'dense', 'syrk+out', '-', 'ext-U'])))
@@ -56,6 +56,7 @@ sel = (ph[:, 0] > 0) & ~issmall
 d = np.diff(ph[sel][:, :7], axis=1) / 1e3
 names = ['zero+K', 'ext-panel', 'dense', 'syrk', 'panel-out', 'ext-U']
 pw = (m * w)[sel]
+chol = (ph[sel][:, 7] - ph[sel][:, 2]) / 1e3
 for lo, hi in [(0, 2000), (2000, 5000), (5000, 1e9)]:
     ss = (pw >= lo) & (pw < hi)
-    print(f"panel [{lo},{hi}) n={ss.sum()} " + ' '.join(f"{nm}={d[ss, k].mean():.1f}" for k, nm in enumerate(names)))
+    print(f"panel [{lo},{hi}) n={ss.sum()} " + ' '.join(f"{nm}={d[ss, k].mean():.1f}" for k, nm in enumerate(names)) + f" (chol+inv {chol[ss].mean():.1f}) mean w {w[sel][ss].mean():.1f}")
