@@ -158,11 +158,14 @@ ckkt_status ckkt_iterate_host(ckkt_ctx *ctx, const double *w_val, const double *
 
 /* Phase profiling (telemetry for the roofline report): when enabled, CUDA events are recorded on
  * the context's stream around every launch of the phases
- *   0 = condensation (k_condense), 1 = numeric factorization, 2 = forward sweeps, 3 = backward sweeps.
+ *   0 = condensation (k_condense), 1 = numeric factorization, 2 = forward sweeps, 3 = backward sweeps,
+ *   4 = vector work of the solve (right-hand side, SpMVs with G / G^T, CG dots and updates, recovery,
+ *       K_aug residuals and refinement updates).
  * ckkt_phase_times synchronises the stream, returns the accumulated device milliseconds and launch
  * counts per phase since the previous call (or since enabling), and resets them. */
 ckkt_status ckkt_profile(ckkt_ctx *ctx, int32_t enable);
-ckkt_status ckkt_phase_times(ckkt_ctx *ctx, double *ms /* [4] */, int64_t *count /* [4] */);
+#define CKKT_NPHASES 5
+ckkt_status ckkt_phase_times(ckkt_ctx *ctx, double *ms /* [CKKT_NPHASES] */, int64_t *count /* [CKKT_NPHASES] */);
 
 /* Number of CUDA kernel launches enqueued by this context since creation (telemetry). */
 int64_t ckkt_launch_count(const ckkt_ctx *ctx);

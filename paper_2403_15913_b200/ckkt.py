@@ -22,7 +22,7 @@ CKKT_LIFTED, CKKT_HYKKT = 0, 1
 EXPORTED = ["ckkt_default_options", "ckkt_setup", "ckkt_get_sizes", "ckkt_export_symbolic", "ckkt_refactor",
             "ckkt_solve", "ckkt_iterate_host", "ckkt_profile", "ckkt_phase_times", "ckkt_launch_count",
             "ckkt_destroy", "ckkt_status_str"]
-PHASES = ("condense", "factor", "forward", "backward")
+PHASES = ("condense", "factor", "forward", "backward", "vector")
 
 
 class ckkt_pattern(ctypes.Structure):
@@ -212,8 +212,8 @@ class Context:
 
     def phase_times(self) -> dict:
         """{phase: (ms, launches)} accumulated since the previous call (synchronises the stream)."""
-        ms = np.zeros(4)
-        cnt = np.zeros(4, np.int64)
+        ms = np.zeros(len(PHASES))
+        cnt = np.zeros(len(PHASES), np.int64)
         rc = lib().ckkt_phase_times(self.h, _np_ptr(ms), _np_ptr(cnt))
         if rc:
             raise CKKTError(rc, "ckkt_phase_times")

@@ -89,6 +89,16 @@ __global__ void k_condense(int64_t nnzk, const int64_t* __restrict__ wt_ptr, con
 
 #include "mf_kernels.cuh"
 
+// out[b][t] = val[b][e[t]]: a transposed copy of G or H values (one pass per refactor), so the
+// column-wise products G^T v / H^T v read their values contiguously
+__global__ void k_gather_t(int64_t nnz, int B, const int32_t* __restrict__ e, const double* __restrict__ val,
+                           double* __restrict__ out) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= nnz * B) return;
+  const int64_t b = t / nnz, k = t - b * nnz;
+  out[t] = val[b * nnz + e[k]];
+}
+
 __global__ void k_init_flags(int B, int* notpd, int* minpiv) {
   int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b < B) { notpd[b] = 0; minpiv[b] = INT_MAX; }
@@ -122,12 +132,12 @@ __global__ void k_rhs(int n, int me, int mi, const int32_t* __restrict__ perm2, 
   for (int t = ht_ptr[j]; t < ht_ptr[j + 1]; ++t) {
     const int r = ht_r[t];
     const int64_t o = (int64_t)b * mi + r;
-    acc += h[ht_e[t]] * (d_s[o] * r4[o] - r2[o]);
+    acc += h[t] * (d_s[o] * r4[o] - r2[o]);
   }
   if (me > 0 && gamma != 0.0) {
     const double* g = g_val + b * g_nnz;
     double sg = 0.0;
-    for (int t = gt_ptr[j]; t < gt_ptr[j + 1]; ++t) sg += g[gt_e[t]] * r3[(int64_t)b * me + gt_r[t]];
+    for (int t = gt_ptr[j]; t < gt_ptr[j + 1]; ++t) sg += g[t] * r3[(int64_t)b * me + gt_r[t]];
     acc += gamma * sg;
   }
   out[(int64_t)b * n + j] = acc;
@@ -143,7 +153,7 @@ __global__ void k_gt_spmv(int n, int me, const int32_t* __restrict__ gt_ptr, con
   if (j >= n || (skip && skip[b])) return;
   const double* g = g_val + b * g_nnz;
   double acc = 0.0;
-  for (int t = gt_ptr[j]; t < gt_ptr[j + 1]; ++t) acc += g[gt_e[t]] * v[(int64_t)b * me + gt_r[t]];
+  for (int t = gt_ptr[j]; t < gt_ptr[j + 1]; ++t) acc += g[t] * v[(int64_t)b * me + gt_r[t]];
   double r = alpha * acc;
   if (z) r += beta * z[(int64_t)b * n + j];
   y[(int64_t)b * n + j] = r;
@@ -184,7 +194,21 @@ __global__ void k_dot_partial(int64_t len, const double* __restrict__ a, const d
   }
 }
 
-constexpr int DOT_BLOCKS = 64;
+constexpr int DOT_BLOCKS = 592;  // 4 per SM: enough loads in flight for the n-long dot products
+
+// fixed-order sum of a block-partials row (four interleaved partial sums)
+__device__ __forceinline__ double sum_parts(const double* __restrict__ p, int nb) {
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int k = 0;
+  for (; k + 3 < nb; k += 4) {
+    s0 += p[k];
+    s1 += p[k + 1];
+    s2 += p[k + 2];
+    s3 += p[k + 3];
+  }
+  for (; k < nb; ++k) s0 += p[k];
+  return (s0 + s1) + (s2 + s3);
+}
 
 // CG scalar step after q = S p:  alpha = rr / (p.q)
 __global__ void k_cg_alpha(int B, const double* __restrict__ part, const double* __restrict__ rr,
@@ -193,7 +217,7 @@ __global__ void k_cg_alpha(int B, const double* __restrict__ part, const double*
   if (b >= B) return;
   if (done[b]) { alpha[b] = 0.0; return; }
   double pq = 0.0;
-  for (int k = 0; k < DOT_BLOCKS; ++k) pq += part[(int64_t)b * DOT_BLOCKS + k];
+  pq = sum_parts(part + (int64_t)b * DOT_BLOCKS, DOT_BLOCKS);
   alpha[b] = rr[b] / pq;
 }
 
@@ -216,7 +240,7 @@ __global__ void k_cg_beta(int B, const double* __restrict__ part, double* __rest
   if (b >= B) return;
   if (done[b]) { beta[b] = 0.0; return; }
   double t = 0.0;
-  for (int k = 0; k < DOT_BLOCKS; ++k) t += part[(int64_t)b * DOT_BLOCKS + k];
+  t = sum_parts(part + (int64_t)b * DOT_BLOCKS, DOT_BLOCKS);
   iters[b] += 1;
   beta[b] = t / rr[b];
   rr[b] = t;
@@ -240,7 +264,7 @@ __global__ void k_cg_init_scalars(int B, const double* __restrict__ part, double
   int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   double t = 0.0;
-  for (int k = 0; k < DOT_BLOCKS; ++k) t += part[(int64_t)b * DOT_BLOCKS + k];
+  t = sum_parts(part + (int64_t)b * DOT_BLOCKS, DOT_BLOCKS);
   rr[b] = t;
   bnorm2[b] = t;
   iters[b] = 0;
@@ -288,6 +312,7 @@ struct ResArgs {
   const int32_t *gt_ptr, *gt_e, *gt_r, *ht_ptr, *ht_e, *ht_r;
   const int32_t *g_rowptr, *g_col2, *h_rowptr, *h_col2;
   const double *w_val, *g_val, *h_val, *sigma, *d_s, *delta;
+  const double *gtv, *htv;  // transposed-order copies
   int64_t w_nnz, g_nnz, h_nnz;
   const double *r1, *r2, *r3, *r4;  // r1 original order
   const double *dx, *ds, *dy, *dz;  // dx internal
@@ -320,17 +345,17 @@ __global__ void k_kaug_residual(ResArgs a) {
     acc += dg;
     aa += fabs(dg);
     if (me) {
-      const double* g = a.g_val + b * a.g_nnz;
+      const double* g = a.gtv + b * a.g_nnz;
       for (int e = a.gt_ptr[i]; e < a.gt_ptr[i + 1]; ++e) {
-        double v = g[a.gt_e[e]] * a.dy[(int64_t)b * me + a.gt_r[e]];
+        double v = g[e] * a.dy[(int64_t)b * me + a.gt_r[e]];
         acc += v;
         aa += fabs(v);
       }
     }
     if (mi) {
-      const double* h = a.h_val + b * a.h_nnz;
+      const double* h = a.htv + b * a.h_nnz;
       for (int e = a.ht_ptr[i]; e < a.ht_ptr[i + 1]; ++e) {
-        double v = h[a.ht_e[e]] * a.dz[(int64_t)b * mi + a.ht_r[e]];
+        double v = h[e] * a.dz[(int64_t)b * mi + a.ht_r[e]];
         acc += v;
         aa += fabs(v);
       }
@@ -492,6 +517,7 @@ struct ckkt_ctx {
   int32_t *chunk_ptr = nullptr, *queue = nullptr, *sub_ptr = nullptr, *sub_nodes = nullptr, *topq = nullptr;
   const SnMeta* qmeta = nullptr;  // metadata of the bottom queue, queue order
   const SnMeta* tmeta = nullptr;  // metadata of the tiny subtrees' nodes, sub_nodes order
+  double *gtv = nullptr, *htv = nullptr;  // G / H values in transposed (column) order, refreshed at refactor
   int ntop = 0;
   const SnMeta* topmeta = nullptr;  // metadata of the top queue, top order
   int topbuf = 0;                   // doubles of the top kernels' panel buffer
@@ -876,6 +902,8 @@ ckkt_status setup_device(ckkt_ctx* c) {
   DALLOC(c->L, (size_t)B * c->Lsize + 4);  // +32 B: 16-byte-rounded L2 prefetches stay in bounds
   DALLOC(c->Ub, (size_t)B * c->Usize);
   DALLOC(c->Vb, (size_t)B * c->Vsize);
+  DALLOC(c->gtv, (size_t)B * std::max<int64_t>(c->g_nnz, 1));
+  DALLOC(c->htv, (size_t)B * std::max<int64_t>(c->h_nnz, 1));
   DALLOC(c->notpd, B);
   DALLOC(c->minpiv, B);
   const size_t Bn = (size_t)B * n, Bme = (size_t)B * std::max(me, 1), Bmi = (size_t)B * std::max(mi, 1);
@@ -1084,7 +1112,7 @@ ckkt_status ckkt_profile(ckkt_ctx* c, int32_t enable) {
 
 ckkt_status ckkt_phase_times(ckkt_ctx* c, double* ms, int64_t* count) {
   if (!c || !c->has_device || !ms || !count) return CKKT_INVALID_ARG;
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < CKKT_NPHASES; ++k) {
     ms[k] = 0.0;
     count[k] = 0;
   }
@@ -1115,6 +1143,14 @@ ckkt_status ckkt_refactor(ckkt_ctx* c, const double* w_val, const double* g_val,
   c->d_s = d_s;
   c->delta = delta_x;
   const double gamma = (c->opt.strategy == CKKT_HYKKT) ? c->opt.gamma : 0.0;
+  if (c->g_nnz) {
+    k_gather_t<<<(unsigned)((c->g_nnz * B + TPB - 1) / TPB), TPB, 0, st>>>(c->g_nnz, B, c->gt_e, g_val, c->gtv);
+    c->launches++;
+  }
+  if (c->h_nnz) {
+    k_gather_t<<<(unsigned)((c->h_nnz * B + TPB - 1) / TPB), TPB, 0, st>>>(c->h_nnz, B, c->ht_e, h_val, c->htv);
+    c->launches++;
+  }
   k_init_flags<<<nblk(B), TPB, 0, st>>>(B, c->notpd, c->minpiv);
   prof_begin(c, 0);
   k_condense<<<dim3(nblk(c->nnzk), B), TPB, 0, st>>>(c->nnzk, c->wt_ptr, c->wt_idx, c->jt_ptr, c->jt_a, c->jt_b,
@@ -1239,15 +1275,18 @@ ckkt_status solve_pass(ckkt_ctx* c, const double* r1, int r1_internal, const dou
   const double gamma = (c->opt.strategy == CKKT_HYKKT) ? c->opt.gamma : 0.0;
   const dim3 gn(nblk(n), B), gme(nblk(std::max(me, 1)), B), gmi(nblk(std::max(mi, 1)), B);
   // r_gamma (or r~) in internal order, into dx (it becomes -K^{-1}(...) after the solves)
+  prof_begin(c, 4);
   k_rhs<<<gn, TPB, 0, st>>>(n, me, mi, c->S.perm2, r1, r1_internal, r2, r3, r4, c->gt_ptr, c->gt_e, c->gt_r,
-                            c->ht_ptr, c->ht_e, c->ht_r, c->g_val, c->g_nnz, c->h_val, c->h_nnz, c->d_s, gamma, c->rg,
+                            c->ht_ptr, c->ht_e, c->ht_r, c->gtv, c->g_nnz, c->htv, c->h_nnz, c->d_s, gamma, c->rg,
                             skip);
   c->launches++;
   kcg.assign(B, 0);
   if (me > 0) {
     // t = K^{-1} r_gamma ; b = r3 - G t
     cudaMemcpyAsync(c->tn, c->rg, sizeof(double) * (size_t)B * n, cudaMemcpyDeviceToDevice, st);
+    prof_end(c);
     ksolve(c, c->tn, skip);
+    prof_begin(c, 4);
     k_g_spmv<<<gme, TPB, 0, st>>>(me, n, c->g_rowptr, c->g_col2, c->g_val, c->g_nnz, c->tn, -1.0, r3, 1.0, c->bvec,
                                   skip);
     // CG: x = 0, r = p = b
@@ -1257,11 +1296,15 @@ ckkt_status solve_pass(ckkt_ctx* c, const double* r1, int r1_internal, const dou
     dot(c, me, c->bvec, c->bvec, skip);
     k_cg_init_scalars<<<nblk(B), TPB, 0, st>>>(B, c->part, c->cg_rr, c->cg_bn, c->cg_done, c->cg_iters, skip);
     c->launches += 4;
+    prof_end(c);
     for (int it = 0; it < c->opt.cg_maxit; ++it) {
       // q = G K^{-1} G^T p
-      k_gt_spmv<<<gn, TPB, 0, st>>>(n, me, c->gt_ptr, c->gt_e, c->gt_r, c->g_val, c->g_nnz, c->cg_p, 1.0, nullptr,
+      prof_begin(c, 4);
+      k_gt_spmv<<<gn, TPB, 0, st>>>(n, me, c->gt_ptr, c->gt_e, c->gt_r, c->gtv, c->g_nnz, c->cg_p, 1.0, nullptr,
                                     0.0, c->vn, c->cg_done);
+      prof_end(c);
       ksolve(c, c->vn, c->cg_done);
+      prof_begin(c, 4);
       k_g_spmv<<<gme, TPB, 0, st>>>(me, n, c->g_rowptr, c->g_col2, c->g_val, c->g_nnz, c->vn, 1.0, nullptr, 0.0,
                                     c->cg_q, c->cg_done);
       dot(c, me, c->cg_p, c->cg_q, c->cg_done);
@@ -1273,16 +1316,19 @@ ckkt_status solve_pass(ckkt_ctx* c, const double* r1, int r1_internal, const dou
                                          c->cg_iters, c->active);
       k_cg_update_p<<<gme, TPB, 0, st>>>(me, c->cg_beta, c->cg_r, c->cg_p, c->cg_done);
       c->launches += 7;
+      prof_end(c);
       int* h_active = c->h_pinned_int + 4 * B;
       CK(cudaMemcpyAsync(h_active, c->active, sizeof(int), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
       if (*h_active == 0) break;
     }
     // dy = x ; dx = K^{-1}(-r_gamma - G^T dy)
+    prof_begin(c, 4);
     cudaMemcpyAsync(dy, c->cg_x, sizeof(double) * (size_t)B * me, cudaMemcpyDeviceToDevice, st);
-    k_gt_spmv<<<gn, TPB, 0, st>>>(n, me, c->gt_ptr, c->gt_e, c->gt_r, c->g_val, c->g_nnz, dy, -1.0, c->rg, -1.0, dx,
+    k_gt_spmv<<<gn, TPB, 0, st>>>(n, me, c->gt_ptr, c->gt_e, c->gt_r, c->gtv, c->g_nnz, dy, -1.0, c->rg, -1.0, dx,
                                   skip);
     c->launches++;
+    prof_end(c);
     ksolve(c, dx, skip);
     int* h_iters = c->h_pinned_int + 3 * B;
     CK(cudaMemcpyAsync(h_iters, c->cg_iters, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
@@ -1291,12 +1337,15 @@ ckkt_status solve_pass(ckkt_ctx* c, const double* r1, int r1_internal, const dou
   } else {
     k_copy_neg<<<gn, TPB, 0, st>>>(n, c->rg, -1.0, dx);
     c->launches++;
+    prof_end(c);
     ksolve(c, dx, skip);
   }
   if (mi > 0) {
+    prof_begin(c, 4);
     k_recover<<<gmi, TPB, 0, st>>>(mi, n, c->h_rowptr, c->h_col2, c->h_val, c->h_nnz, dx, r2, r4, c->d_s, ds, dz,
                                    skip);
     c->launches++;
+    prof_end(c);
   }
   CK(cudaGetLastError());
   return CKKT_OK;
@@ -1316,6 +1365,7 @@ void residual(ckkt_ctx* c, const double* r1, const double* r2, const double* r3,
   a.ht_ptr = c->ht_ptr; a.ht_e = c->ht_e; a.ht_r = c->ht_r;
   a.g_rowptr = c->g_rowptr; a.g_col2 = c->g_col2; a.h_rowptr = c->h_rowptr; a.h_col2 = c->h_col2;
   a.w_val = c->w_val; a.g_val = c->g_val; a.h_val = c->h_val; a.sigma = c->sigma; a.d_s = c->d_s; a.delta = c->delta;
+  a.gtv = c->gtv; a.htv = c->htv;
   a.w_nnz = c->w_nnz; a.g_nnz = c->g_nnz; a.h_nnz = c->h_nnz;
   a.r1 = r1; a.r2 = r2; a.r3 = r3; a.r4 = r4;
   a.dx = dx; a.ds = ds; a.dy = dy; a.dz = dz;
@@ -1323,12 +1373,14 @@ void residual(ckkt_ctx* c, const double* r1, const double* r2, const double* r3,
   a.ratio = c->ratio; a.absres = c->absres;
   a.skip = c->notpd;
   cudaStream_t st = c->stream;
+  prof_begin(c, 4);
   k_kaug_residual<<<dim3(nblk(rows), B), TPB, 0, st>>>(a);
   k_max_partial<<<dim3(DOT_BLOCKS, B), TPB, 0, st>>>(rows, c->ratio, c->part);
   k_max_final<<<nblk(B), TPB, 0, st>>>(B, DOT_BLOCKS, c->part, omega);
   k_max_partial<<<dim3(DOT_BLOCKS, B), TPB, 0, st>>>(rows, c->absres, c->part);
   k_max_final<<<nblk(B), TPB, 0, st>>>(B, DOT_BLOCKS, c->part, resinf);
   c->launches += 5;
+  prof_end(c);
 }
 
 }  // namespace
@@ -1368,6 +1420,7 @@ extern "C" ckkt_status ckkt_solve(ckkt_ctx* c, const double* r1, const double* r
     for (int b = 0; b < B; ++b) h_skip[b] = done[b];
     CK(cudaMemcpyAsync(c->skipflag, h_skip, sizeof(int) * B, cudaMemcpyHostToDevice, st));
     // correction: solve K_aug delta = rho  (i.e. right-hand side "r" = -rho)
+    prof_begin(c, 4);
     k_copy_neg<<<gn, TPB, 0, st>>>(n, c->rho1, -1.0, c->rho1b);
     if (mi) {
       k_copy_neg<<<gmi, TPB, 0, st>>>(mi, c->rho2, -1.0, c->rho2b);
@@ -1375,9 +1428,11 @@ extern "C" ckkt_status ckkt_solve(ckkt_ctx* c, const double* r1, const double* r
     }
     if (me) k_copy_neg<<<gme, TPB, 0, st>>>(me, c->rho3, -1.0, c->rho3b);
     c->launches += 4;
+    prof_end(c);
     s = solve_pass(c, c->rho1b, 1, c->rho2b, c->rho3b, c->rho4b, c->cdx, c->cds, c->cdy, c->cdz, c->skipflag, kcg);
     if (s != CKKT_OK) return s;
     // trial = d + correction
+    prof_begin(c, 4);
     k_axpy_sel<<<gn, TPB, 0, st>>>(n, c->dxi, c->cdx, c->dxi2);
     if (mi) {
       k_axpy_sel<<<gmi, TPB, 0, st>>>(mi, ds, c->cds, c->ds2);
@@ -1385,6 +1440,7 @@ extern "C" ckkt_status ckkt_solve(ckkt_ctx* c, const double* r1, const double* r
     }
     if (me) k_axpy_sel<<<gme, TPB, 0, st>>>(me, dy, c->cdy, c->dy2);
     c->launches += 4;
+    prof_end(c);
     residual(c, r1, r2, r3, r4, c->dxi2, c->ds2, c->dy2, c->dz2, c->rho1b, c->rho2b, c->rho3b, c->rho4b,
              c->omega + B, c->resinf + B);
     CK(cudaMemcpyAsync(c->h_pinned_dbl + 2 * B, c->omega + B, sizeof(double) * B, cudaMemcpyDeviceToHost, st));
@@ -1407,6 +1463,7 @@ extern "C" ckkt_status ckkt_solve(ckkt_ctx* c, const double* r1, const double* r
       c->h_pinned_int[2 * B + b] = acc;
     }
     CK(cudaMemcpyAsync(c->accflag, c->h_pinned_int + 2 * B, sizeof(int) * B, cudaMemcpyHostToDevice, st));
+    prof_begin(c, 4);
     k_copy_sel<<<gn, TPB, 0, st>>>(n, c->dxi2, c->dxi, c->accflag);
     k_copy_sel<<<gn, TPB, 0, st>>>(n, c->rho1b, c->rho1, c->accflag);
     if (mi) {
@@ -1420,7 +1477,9 @@ extern "C" ckkt_status ckkt_solve(ckkt_ctx* c, const double* r1, const double* r
       k_copy_sel<<<gme, TPB, 0, st>>>(me, c->rho3b, c->rho3, c->accflag);
     }
     c->launches += 8;
+    prof_end(c);
   }
+  prof_begin(c, 4);
   k_unpermute<<<gn, TPB, 0, st>>>(n, c->S.perm2, c->dxi, dx, c->notpd);
   if (mi) {
     k_nan_fill<<<gmi, TPB, 0, st>>>(mi, ds, c->notpd);
@@ -1428,6 +1487,7 @@ extern "C" ckkt_status ckkt_solve(ckkt_ctx* c, const double* r1, const double* r
   }
   if (me) k_nan_fill<<<gme, TPB, 0, st>>>(me, dy, c->notpd);
   c->launches += 4;
+  prof_end(c);
   CK(cudaGetLastError());
   ckkt_status worst = CKKT_OK;
   if (info) {

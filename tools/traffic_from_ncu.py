@@ -13,10 +13,10 @@ for row in r[2:]:
     name = d['Kernel Name'].split('(')[0].replace('<unnamed>::', '')
     tot = sum(float(d[k].replace(',', '')) * scale[u[k]] for k in ('dram__bytes_read.sum', 'dram__bytes_write.sum'))
     per.setdefault(name, tot)  # first capture of each kernel
-fwd = per['k_fwd_tiny'] + per['k_fwd_persist']
-bwd = per['k_bwd_persist'] + per['k_bwd_tiny']
-res = {"_source": note, "k_fwd_tiny + k_fwd_persist (one forward sweep)": fwd,
-       "k_bwd_persist + k_bwd_tiny (one backward sweep)": bwd, "k_factor_persist": per['k_factor_persist'],
+fwd = per['k_fwd_tiny'] + per['k_fwd_persist'] + per.get('k_fwd_top', 0.0)
+bwd = per.get('k_bwd_top', 0.0) + per['k_bwd_persist'] + per['k_bwd_tiny']
+res = {"_source": note, "k_fwd_tiny + k_fwd_persist + k_fwd_top (one forward sweep)": fwd,
+       "k_bwd_top + k_bwd_persist + k_bwd_tiny (one backward sweep)": bwd, "k_factor_persist": per['k_factor_persist'],
        "_per_kernel": per}
 json.dump(res, open('profiles/traffic.json', 'w'), indent=1)
 print(json.dumps(res, indent=1))
