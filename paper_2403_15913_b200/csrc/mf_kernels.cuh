@@ -157,36 +157,44 @@ __device__ __forceinline__ int next_ticket(int* ctr_slot, int* sh) {
 // Extend-add of child c's update matrix U_c (mc x mc, lower, column-major) into the parent front:
 //   part 0: columns j < relw (targets in the parent's panel, shared memory Ps with leading dim ldp)
 //   part 1: columns j >= relw (targets in the parent's update block U, global, leading dim mu)
-// Flat iteration over U_c's column-major elements with 8 independent source (and target) loads per
-// thread per batch; targets of one child are distinct, so there are no races within a child.
+// Only the lower triangle is visited: warps take columns (4 per batch, so every lane keeps 4
+// independent loads in flight), lanes take rows i >= j of those columns; rel[j] is uniform per
+// column.  Targets of one child are distinct, so there are no races within a child.
 template <int PART>
 __device__ __forceinline__ void extend_add(const double* __restrict__ Uc, int mc, int relw,
                                            const int32_t* __restrict__ rel, int w, double* Ps, int ldp, double* U,
                                            int mu, int tid, int nt) {
-  const int e_lo = PART == 0 ? 0 : relw * mc;
-  const int e_hi = PART == 0 ? relw * mc : mc * mc;
-  for (int e0 = e_lo; e0 < e_hi; e0 += 8 * nt) {
-    double sv[8], tv[8];
-    int tgt[8];
+  const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  const int j_lo = PART == 0 ? 0 : relw, j_hi = PART == 0 ? relw : mc;
+  for (int j0 = j_lo + wid; j0 < j_hi; j0 += 4 * nw) {
+    int rj[4];
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const int e = e0 + r * nt + tid;
-      const int j = e / mc, i = e - j * mc;
-      const bool ok = e < e_hi && i >= j;
-      sv[r] = ok ? __ldcg(Uc + e) : 0.0;
-      if (ok) {
-        const int ri = __ldg(rel + i), rj = __ldg(rel + j);
-        tgt[r] = PART == 0 ? ri + rj * ldp : (ri - w) + (rj - w) * mu;
-      } else {
-        tgt[r] = -1;
-      }
-      if (PART == 1) tv[r] = (tgt[r] >= 0) ? U[tgt[r]] : 0.0;
+    for (int q = 0; q < 4; ++q) {
+      const int j = j0 + q * nw;
+      rj[q] = (j < j_hi) ? __ldg(rel + j) : 0;
     }
+    for (int r0 = 0; j0 + r0 < mc; r0 += 32) {  // column j0 is the longest of the batch
+      double sv[4], tv[4];
+      int tgt[4];
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      if (tgt[r] < 0) continue;
-      if (PART == 0) Ps[tgt[r]] += sv[r];
-      else U[tgt[r]] = tv[r] + sv[r];
+      for (int q = 0; q < 4; ++q) {
+        const int j = j0 + q * nw, i = j + r0 + lane;
+        const bool ok = j < j_hi && i < mc;
+        sv[q] = ok ? __ldcg(Uc + i + (int64_t)j * mc) : 0.0;
+        if (ok) {
+          const int ri = __ldg(rel + i);
+          tgt[q] = PART == 0 ? ri + rj[q] * ldp : (ri - w) + (rj[q] - w) * mu;
+        } else {
+          tgt[q] = -1;
+        }
+        if (PART == 1) tv[q] = (tgt[q] >= 0) ? U[tgt[q]] : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (tgt[q] < 0) continue;
+        if (PART == 0) Ps[tgt[q]] += sv[q];
+        else U[tgt[q]] = tv[q] + sv[q];
+      }
     }
   }
 }
