@@ -10,7 +10,7 @@ CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 LIB = os.path.join(HERE, "libckkt.so")
 SOURCES = ["analysis.cpp", "ckkt.cu"]
-HEADERS = ["analysis.h", "mf_kernels.cuh", os.path.join(INCLUDE, "ckkt.h")]
+HEADERS = ["analysis.h", "mf_kernels.cuh", "dense_front.cuh", os.path.join(INCLUDE, "ckkt.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-O3", "--expt-relaxed-constexpr"]

@@ -19,6 +19,8 @@
 // with ld.global.cg (L2) so that stale L1 lines are never used.
 // Everything is deterministic: children are assembled in a fixed order, no value atomics.
 
+#include "dense_front.cuh"
+
 constexpr int SMALL_PANEL = 512;   // doubles of a small supernode panel (m * w)
 constexpr int SMALL_WARPS = 8;     // warps per CTA; small supernodes per task
 constexpr int MF_THREADS = 32 * SMALL_WARPS;
@@ -369,7 +371,7 @@ __device__ void factor_big(const SymDev& S, int s, int b, double* Ps, double* ds
     __syncthreads();
   }
   if (ph) ph[2] = gtimer();
-  DENSE_FRONT(__syncthreads)
+  dfront::cta_dense_blocked(Ps, ldp, w, m, tid, nt, dsh, notpd + b, minpiv + b, f);  // [Z; L21]
   if (ph) ph[3] = gtimer();
   {  // U_s = -L21 L21^T: 8x8 DMMA tiles of the lower triangle (Z's upper part is zero, pads are zero)
     const int nb = (mu + 7) >> 3;

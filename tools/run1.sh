@@ -1,2 +1,3 @@
 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; tail -1 gpurun_out/pytest_gpu.log
-python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e --no-lifted > gpurun_out/b3.json 2> gpurun_out/b3.err; python -c "import json; d=json.load(open('gpurun_out/b3.json')); print(d['value'], d['phases_ms'], d['roofline']['phases_ms_per_step'], d['roofline']['launches_per_step'], d['gpu_launches']/d['steps'])"
+python tools/time_solve.py 5000:1072 50000:1072
+python tools/trace_fac.py 50000 1072 2>&1 | grep "panel \["
