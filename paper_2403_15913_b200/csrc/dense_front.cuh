@@ -98,10 +98,17 @@ __device__ __forceinline__ void warp_chol_inv16(double* D, int ld, int bw, int l
 // C (8 x 8 tile at rows r0.., columns c0.. of the panel) op= A B^T or A B with fragments read from
 // shared memory by callers; helpers below are written out per phase for clarity.
 
-// Dense part of a front (see the header comment).  Ps: panel, ldp, w (<= 64), m; dsh >= 17 *
-// nwarp doubles of scratch; all threads of the CTA call it.
-__device__ __forceinline__ void cta_dense_blocked(double* Ps, int ldp, int w, int m, int tid, int nt, double* scr,
-                                                  int* notpd, int* minpiv, int f) {
+// Dense part of a front (see the header comment).  Ps: panel, ldp, w (<= 64), m; scr >= 17
+// doubles of scratch; all nt threads of the group (the CTA, or one warp with nt = 32) call it.
+template <bool CTA>  // CTA: all warps of the block (__syncthreads); else one warp alone (__syncwarp)
+__device__ __forceinline__ void group_sync() {
+  if (CTA) __syncthreads();
+  else __syncwarp();
+}
+
+template <bool CTA>
+__device__ __forceinline__ void dense_blocked(double* Ps, int ldp, int w, int m, int tid, int nt, double* scr,
+                                              int* notpd, int* minpiv, int f) {
   const int lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
   const int g = lane >> 2, t4 = lane & 3;
   const int nb = (w + NBW - 1) / NBW;
@@ -109,7 +116,7 @@ __device__ __forceinline__ void cta_dense_blocked(double* Ps, int ldp, int w, in
     const int o = NBW * kb, bw = min(NBW, w - o);
     // (a) diagonal block
     if (warp == 0) warp_chol_inv16(Ps + o + o * ldp, ldp, bw, lane, scr, notpd, minpiv, f + o);
-    __syncthreads();
+    group_sync<CTA>();
     const int r0 = o + bw;  // first row below the block
     const int nI = (m - r0 + 7) >> 3;
     // (b) L[r, blk] = A[r, blk] Zd^T for r >= r0 (a warp owns whole 8-row tiles: in place)
@@ -137,7 +144,7 @@ __device__ __forceinline__ void cta_dense_blocked(double* Ps, int ldp, int w, in
         }
       }
     }
-    __syncthreads();
+    group_sync<CTA>();
     // (c) trailing update of columns c >= r0 (< w), rows r >= r0: A[r, c] -= L[r, blk] L[c, blk]^T
     if (r0 < w) {
       const int nJ = (w - r0 + 7) >> 3;
@@ -159,7 +166,7 @@ __device__ __forceinline__ void cta_dense_blocked(double* Ps, int ldp, int w, in
           if (col + 1 < w) Ps[row + (col + 1) * ldp] -= c1;
         }
       }
-      __syncthreads();
+      group_sync<CTA>();
     }
   }
   // (d) Z from the inverted diagonal blocks: Z_ij = -Zd_i sum_{k=j}^{i-1} L_ik Z_kj  (i > j)
@@ -188,7 +195,7 @@ __device__ __forceinline__ void cta_dense_blocked(double* Ps, int ldp, int w, in
         }
       }
     }
-    __syncthreads();  // every T of block row bi computed before any L_ij is replaced
+    group_sync<CTA>();  // every T of block row bi computed before any L_ij is replaced
     for (int q = 0; q < 2; ++q) {
       const int tI = warp + q * nwarp;
       if (tI < ntile) {
@@ -200,7 +207,7 @@ __device__ __forceinline__ void cta_dense_blocked(double* Ps, int ldp, int w, in
         }
       }
     }
-    __syncthreads();
+    group_sync<CTA>();
     // Z_ij = -Zd_i T_ij  (A = Zd_i lower with zero upper part, B = T not transposed)
     for (int q = 0; q < 2; ++q) {
       const int tI = warp + q * nwarp;
@@ -217,7 +224,7 @@ __device__ __forceinline__ void cta_dense_blocked(double* Ps, int ldp, int w, in
         }
       }
     }
-    __syncthreads();
+    group_sync<CTA>();
     for (int q = 0; q < 2; ++q) {
       const int tI = warp + q * nwarp;
       if (tI < ntile) {
@@ -229,14 +236,14 @@ __device__ __forceinline__ void cta_dense_blocked(double* Ps, int ldp, int w, in
         }
       }
     }
-    __syncthreads();
+    group_sync<CTA>();
   }
   // (e) clear the strict upper triangle of the w x w block (trailing-update tiles straddled it)
   for (int p = tid; p < w * w; p += nt) {
     const int i = p % w, c = p / w;
     if (i < c) Ps[i + c * ldp] = 0.0;
   }
-  __syncthreads();
+  group_sync<CTA>();
 }
 
 }  // namespace dfront

@@ -201,112 +201,6 @@ __device__ __forceinline__ void extend_add(const double* __restrict__ Uc, int mc
   }
 }
 
-// L21 <- A21 Z^T in place (Z = L11^{-1}, lower triangular, w x w at the top of the panel; A21 = rows
-// w..m-1), with FP64 tensor-core tiles mma.m8n8k4.  Warp `warp` of `nwarp` owns the 8-row tiles
-// I = warp, warp + nwarp, ...: it accumulates every 8-column tile of its rows in registers before
-// writing any of them back, so the in-place update never reads a value another warp has replaced.
-// Fragments outside the w columns / m rows are zeroed (the panel need not be padded).
-__device__ __forceinline__ void warp_trsm_dmma(double* Ps, int ldp, int w, int m, int warp, int nwarp, int lane) {
-  const int mu = m - w, g = lane >> 2, t4 = lane & 3;
-  const int nI = (mu + 7) >> 3, nJ = (w + 7) >> 3;
-  for (int I = warp; I < nI; I += nwarp) {
-    const int ra = w + 8 * I + g;  // A21 row of this lane's A fragment
-    double c[16];
-#pragma unroll
-    for (int q = 0; q < 16; ++q) c[q] = 0.0;
-    for (int k = 0; k < w; k += 4) {
-      const int kc = k + t4;
-      const double a = (ra < m && kc < w) ? Ps[ra + kc * ldp] : 0.0;
-#pragma unroll
-      for (int J = 0; J < 8; ++J) {
-        if (J < nJ && k < 8 * J + 8) {  // Z[j][k] = 0 for k > j
-          const int rb = 8 * J + g;
-          const double bv = (rb < w && kc < w) ? Ps[rb + kc * ldp] : 0.0;
-          dmma_8x8x4(c[2 * J], c[2 * J + 1], a, bv);
-        }
-      }
-    }
-    __syncwarp();
-    const int row = w + 8 * I + g;
-    if (row < m) {
-#pragma unroll
-      for (int J = 0; J < 8; ++J) {
-        const int col = 8 * J + 2 * t4;
-        if (J < nJ) {
-          if (col < w) Ps[row + col * ldp] = c[2 * J];
-          if (col + 1 < w) Ps[row + (col + 1) * ldp] = c[2 * J + 1];
-        }
-      }
-    }
-  }
-}
-
-// One warp: A11 (w x w, w <= 64, lower part of the panel top) <- Z = L11^{-1} where L11 = chol(A11).
-// Lanes own rows lane and lane + 32.  Cholesky is left-looking (Crout): column j of L is a dot
-// product over the finished columns k < j, so each step only loads from shared memory and stores
-// one value per row (no read-after-write chains through shared memory).  Reciprocal pivots are
-// kept in dsh[] and reused by the inversion, which runs row by row (row i of Z from rows < i).
-__device__ __forceinline__ void warp_chol_inv(double* Ps, int ldp, int w, int lane, double* dsh, int* notpd_b,
-                                              int* minpiv_b, int f) {
-  const int i0 = lane, i1 = lane + 32;
-  for (int j = 0; j < w; ++j) {
-    double s0 = 0.0, s1 = 0.0;
-    const bool a0 = i0 >= j && i0 < w, a1 = i1 >= j && i1 < w;
-    if (a0) s0 = Ps[i0 + j * ldp];
-    if (a1) s1 = Ps[i1 + j * ldp];
-    for (int k = 0; k < j; ++k) {
-      const double ljk = Ps[j + k * ldp];
-      if (a0) s0 -= Ps[i0 + k * ldp] * ljk;
-      if (a1) s1 -= Ps[i1 + k * ldp] * ljk;
-    }
-    if (i0 == j || i1 == j) {
-      double d = (i0 == j) ? s0 : s1;
-      if (!(d > 0.0) || !isfinite(d)) {
-        *notpd_b = 1;
-        atomicMin(minpiv_b, f + j);
-        d = nan("");
-      }
-      const double piv = sqrt(d);
-      Ps[j + j * ldp] = piv;
-      dsh[j] = 1.0 / piv;
-    }
-    __syncwarp();
-    const double rp = dsh[j];
-    if (a0 && i0 > j) Ps[i0 + j * ldp] = s0 * rp;
-    if (a1 && i1 > j) Ps[i1 + j * ldp] = s1 * rp;
-    __syncwarp();
-  }
-  for (int i = 0; i < w; ++i) {  // Z = L11^{-1}: row i from rows < i
-    double z0 = 0.0, z1 = 0.0;
-    const double ri = dsh[i];
-    if (lane <= i) {
-      z0 = (lane == i) ? 1.0 : 0.0;
-      for (int k = lane; k < i; ++k) z0 -= Ps[i + k * ldp] * Ps[k + lane * ldp];
-      z0 *= ri;
-    }
-    if (lane + 32 <= i) {
-      z1 = (lane + 32 == i) ? 1.0 : 0.0;
-      for (int k = lane + 32; k < i; ++k) z1 -= Ps[i + k * ldp] * Ps[k + (lane + 32) * ldp];
-      z1 *= ri;
-    }
-    __syncwarp();
-    if (lane <= i) Ps[i + lane * ldp] = z0;
-    if (lane + 32 <= i) Ps[i + (lane + 32) * ldp] = z1;
-    __syncwarp();
-  }
-}
-
-// Dense part of a front on the panel in shared memory (ld = ldp), by ONE warp for the w x w block
-// (w <= 64, lanes own rows lane and lane + 32), then all warps of the group for the rows below:
-//   L11 = chol(A11) (column by column, warp-synchronous), Z = L11^{-1} (row by row), L21 = A21 Z^T
-//   (DMMA tiles, warp_trsm_dmma).
-// Returns with Ps holding [Z; L21].  GROUP_SYNC() synchronises the whole group.
-#define DENSE_FRONT(GROUP_SYNC)                                                                         \
-  if (tid < 32) warp_chol_inv(Ps, ldp, w, tid, dsh, notpd + b, minpiv + b, f);                       \
-  GROUP_SYNC();                                                                                       \
-  warp_trsm_dmma(Ps, ldp, w, m, tid >> 5, nt >> 5, tid & 31); /* L21 = A21 Z^T (FP64 DMMA tiles) */    \
-  GROUP_SYNC();
-
 // small supernode, one warp, panel in shared memory (ld = m)
 __device__ void factor_small(const SymDev& S, int s, int b, int tid, double* Ps, double* dsh, double* L, int64_t Lsize,
                              double* Ub, int64_t Usize, const double* __restrict__ Kb, int* notpd, int* minpiv) {
@@ -326,7 +220,7 @@ __device__ void factor_small(const SymDev& S, int s, int b, int tid, double* Ps,
                   mu, tid, nt);
     __syncwarp();
   }
-  DENSE_FRONT(__syncwarp)
+  dfront::dense_blocked<false>(Ps, ldp, w, m, tid, nt, dsh, notpd + b, minpiv + b, f);  // [Z; L21]
   for (int i = tid; i < m * w; i += nt) P[i] = Ps[i];
   for (int j = 0; j < mu; ++j)  // U_s = -L21 L21^T (lower)
     for (int i = j + tid; i < mu; i += nt) {
@@ -371,7 +265,7 @@ __device__ void factor_big(const SymDev& S, int s, int b, double* Ps, double* ds
     __syncthreads();
   }
   if (ph) ph[2] = gtimer();
-  dfront::cta_dense_blocked(Ps, ldp, w, m, tid, nt, dsh, notpd + b, minpiv + b, f);  // [Z; L21]
+  dfront::dense_blocked<true>(Ps, ldp, w, m, tid, nt, dsh, notpd + b, minpiv + b, f);  // [Z; L21]
   if (ph) ph[3] = gtimer();
   {  // U_s = -L21 L21^T: 8x8 DMMA tiles of the lower triangle (Z's upper part is zero, pads are zero)
     const int nb = (mu + 7) >> 3;
