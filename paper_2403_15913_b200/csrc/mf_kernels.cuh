@@ -97,7 +97,7 @@ __device__ __forceinline__ int ld_relaxed(const int* p) {
 }
 
 #ifndef CKKT_POLL_MAX_NS
-#define CKKT_POLL_MAX_NS 256
+#define CKKT_POLL_MAX_NS 64
 #endif
 // Poll with relaxed loads.  Everything a consumer reads from another CTA after the wait (children's
 // update matrices / vectors, the solution entries of ancestors) is read with ld.global.cg, i.e. from
