@@ -1164,9 +1164,8 @@ ckkt_status ckkt_refactor(ckkt_ctx* c, const double* w_val, const double* g_val,
   ++c->epoch_fac;
   prof_begin(c, 1);
   if (c->nsub > 0)
-    k_factor_tiny<<<(c->nsub * B + 127) / 128, 128, 0, st>>>(c->S, c->sub_ptr, c->sub_nodes, c->nsub, B, c->L,
-                                                              c->Lsize, c->Ub, c->Usize, c->Kval, c->nnzk, c->notpd,
-                                                              c->minpiv);
+    k_factor_tiny<<<(c->nsub * B * TG + FT_THREADS - 1) / FT_THREADS, FT_THREADS, 0, st>>>(
+        c->S, c->tmeta, c->sub_ptr, c->nsub, B, c->L, c->Lsize, c->Ub, c->Usize, c->Kval, c->nnzk, c->notpd, c->minpiv);
   DBG_SYNC("k_factor_tiny");
   if (c->ntask > 0)
     k_factor_persist<<<c->grid_fac, MF_THREADS, c->fac_smem, st>>>(c->S, c->Qfac, A.ns, B, c->epoch_fac, c->L,

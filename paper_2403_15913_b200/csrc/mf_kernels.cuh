@@ -1236,73 +1236,115 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-__global__ void __launch_bounds__(128)
-    k_factor_tiny(SymDev S, const int32_t* __restrict__ sub_ptr, const int32_t* __restrict__ sub_nodes, int nsub,
-                  int B, double* L, int64_t Lsize, double* Ub, int64_t Usize, const double* __restrict__ Kval,
-                  int64_t nnzk, int* notpd, int* minpiv) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nsub * B) return;
-  const int sub = t / B, b = t % B;
+// Factor of the tiny subtrees: a group of TG lanes per (subtree, instance), nodes in postorder,
+// front panel (m <= 32 rows, w <= 4 columns, ld 32) in the group's shared memory, rows over lanes.
+// Same arithmetic as the big fronts: assemble A + children's panel parts, Cholesky of
+// the w columns, U_s = -L21 L21^T plus the children's trailing parts, L11 <- L11^{-1}.
+constexpr int FT_THREADS = 256;
+__global__ void __launch_bounds__(FT_THREADS)
+    k_factor_tiny(SymDev S, const SnMeta* __restrict__ tmeta, const int32_t* __restrict__ sub_ptr, int nsub, int B,
+                  double* L, int64_t Lsize, double* Ub, int64_t Usize, const double* __restrict__ Kval, int64_t nnzk,
+                  int* notpd, int* minpiv) {
+  constexpr int LD = 32;
+  __shared__ double pan_all[FT_THREADS / TG][LD * TINY_W];
+  const int gid = (blockIdx.x * blockDim.x + threadIdx.x) / TG, g = threadIdx.x % TG;
+  if (gid >= nsub * B) return;  // group-uniform
+  const unsigned mask = (TG == 32 ? 0xFFFFFFFFu : ((1u << TG) - 1u)) << ((threadIdx.x & 31) & ~(TG - 1));
+  const int sub = gid / B, b = gid % B;
+  double* Pn = pan_all[threadIdx.x / TG];
   const double* Kb = Kval + b * nnzk;
   double* Ubb = Ub + b * Usize;
-  for (int q = sub_ptr[sub]; q < sub_ptr[sub + 1]; ++q) {
-    const int s = sub_nodes[q];
-    const int f = S.sfirst[s], w = S.sfirst[s + 1] - f;
-    const int m = (int)(S.srowptr[s + 1] - S.srowptr[s]);
-    const int mu = m - w;
-    double P[TINY_M * TINY_W];
-    for (int i = 0; i < m * w; ++i) P[i] = 0.0;
-    for (int64_t k = S.kp[f]; k < S.kp[f + w]; ++k) P[S.kmap[k]] = Kb[k];
-    for (int ci = S.ch_ptr[s]; ci < S.ch_ptr[s + 1]; ++ci) {  // panel part of the children
-      const int c = S.ch_list[ci];
-      const int mc = off_rows(S, c);
-      const double* Uc = Ubb + S.uofs[c];
-      const int32_t* rel = S.relmap + S.relofs[c];
-      for (int j = 0; j < mc && rel[j] < w; ++j)
-        for (int i = j; i < mc; ++i) P[rel[i] + rel[j] * m] += Uc[i + j * mc];
+  const int q1 = sub_ptr[sub + 1];
+  for (int q = sub_ptr[sub]; q < q1; ++q) {
+    const SnMeta M = tmeta[q];
+    const int f = M.f, w = M.w, m = M.m, mu = m - w;
+    // (1) A's entries of the w columns (kmap is relative to the m x w panel with ld m)
+    for (int e = g; e < LD * TINY_W; e += TG) Pn[e] = 0.0;
+    __syncwarp(mask);
+    for (int64_t k = S.kp[f] + g; k < S.kp[f + w]; k += TG) {
+      const int qq = S.kmap[k];
+      Pn[(qq % m) + (qq / m) * LD] = Kb[k];
     }
-    for (int j = 0; j < w; ++j) {  // Cholesky of the first w columns
-      double d = P[j + j * m];
+    __syncwarp(mask);
+    // (2) children's panel parts (columns j with rel[j] < w), child by child
+    for (int ci = M.ch0; ci < M.ch1; ++ci) {
+      const ChMeta cm = S.chmeta[ci];
+      const double* Uc = Ubb + S.uofs[cm.c];
+      const int32_t* rel = S.relmap + cm.relofs;
+      for (int j = 0; j < cm.mc; ++j) {
+        const int rj = __ldg(rel + j);
+        if (rj >= w) break;
+        for (int i = j + g; i < cm.mc; i += TG) Pn[__ldg(rel + i) + rj * LD] += __ldcg(Uc + i + j * cm.mc);
+      }
+      __syncwarp(mask);
+    }
+    // (3) Cholesky of the w columns (rows over lanes)
+    for (int j = 0; j < w; ++j) {
+      double d = Pn[j + j * LD];
       if (!(d > 0.0) || !isfinite(d)) {
-        notpd[b] = 1;
-        atomicMin(&minpiv[b], f + j);
+        if (g == 0) {
+          notpd[b] = 1;
+          atomicMin(&minpiv[b], f + j);
+        }
         d = nan("");
       }
-      const double piv = sqrt(d);
-      P[j + j * m] = piv;
-      for (int i = j + 1; i < m; ++i) P[i + j * m] /= piv;
+      const double rp = 1.0 / sqrt(d);
+      __syncwarp(mask);
+      for (int i = j + 1 + g; i < m; i += TG) Pn[i + j * LD] *= rp;
+      if (g == 0) Pn[j + j * LD] = d * rp;
+      __syncwarp(mask);
       for (int c2 = j + 1; c2 < w; ++c2) {
-        const double lc = P[c2 + j * m];
-        for (int i = c2; i < m; ++i) P[i + c2 * m] -= P[i + j * m] * lc;
+        const double lc = Pn[c2 + j * LD];
+        for (int i = c2 + g; i < m; i += TG) Pn[i + c2 * LD] -= Pn[i + j * LD] * lc;
       }
+      __syncwarp(mask);
     }
-    double* U = Ubb + S.uofs[s];
-    for (int j = 0; j < mu; ++j)  // U_s = -L21 L21^T (lower)
-      for (int i = j; i < mu; ++i) {
+    // (4) U_s = -L21 L21^T (lower, column-major mu x mu), then the children's trailing parts
+    double* U = Ubb + S.uofs[M.pad1];  // (tmeta: pad1 = supernode)
+    for (int j = 0; j < mu; ++j)
+      for (int i = j + g; i < mu; i += TG) {
         double acc = 0.0;
-        for (int k = 0; k < w; ++k) acc += P[w + i + k * m] * P[w + j + k * m];
+#pragma unroll
+        for (int k = 0; k < TINY_W; ++k)
+          if (k < w) acc += Pn[w + i + k * LD] * Pn[w + j + k * LD];
         U[i + j * mu] = -acc;
       }
-    for (int ci = S.ch_ptr[s]; ci < S.ch_ptr[s + 1]; ++ci) {  // trailing part of the children
-      const int c = S.ch_list[ci];
-      const int mc = off_rows(S, c);
-      const double* Uc = Ubb + S.uofs[c];
-      const int32_t* rel = S.relmap + S.relofs[c];
-      for (int j = 0; j < mc; ++j) {
-        if (rel[j] < w) continue;
-        for (int i = j; i < mc; ++i) U[(rel[i] - w) + (rel[j] - w) * mu] += Uc[i + j * mc];
+    __syncwarp(mask);
+    for (int ci = M.ch0; ci < M.ch1; ++ci) {
+      const ChMeta cm = S.chmeta[ci];
+      const double* Uc = Ubb + S.uofs[cm.c];
+      const int32_t* rel = S.relmap + cm.relofs;
+      for (int j = 0; j < cm.mc; ++j) {
+        const int rj = __ldg(rel + j);
+        if (rj < w) continue;
+        for (int i = j + g; i < cm.mc; i += TG) U[(__ldg(rel + i) - w) + (rj - w) * mu] += __ldcg(Uc + i + j * cm.mc);
       }
+      __syncwarp(mask);
     }
-    for (int i = 0; i < w; ++i) {  // L11 <- L11^{-1}, row by row
+    // (5) L11 <- L11^{-1} (w <= 4): lane i < w computes row i from rows < i, one row per step
+    for (int i = 0; i < w; ++i) {
       double z[TINY_W];
-      for (int j = 0; j <= i; ++j) {
-        double acc = (j == i) ? 1.0 : 0.0;
-        for (int k = j; k < i; ++k) acc -= P[i + k * m] * P[k + j * m];
-        z[j] = acc / P[i + i * m];
+#pragma unroll
+      for (int jj = 0; jj < TINY_W; ++jj) z[jj] = 0.0;
+      if (g == 0) {
+        const double rii = 1.0 / Pn[i + i * LD];
+#pragma unroll
+        for (int jj = 0; jj < TINY_W; ++jj) {
+          if (jj <= i) {
+            double acc = (jj == i) ? 1.0 : 0.0;
+            for (int k = jj; k < i; ++k) acc -= Pn[i + k * LD] * Pn[k + jj * LD];
+            z[jj] = acc * rii;
+          }
+        }
+#pragma unroll
+        for (int jj = 0; jj < TINY_W; ++jj)
+          if (jj <= i) Pn[i + jj * LD] = z[jj];
       }
-      for (int j = 0; j <= i; ++j) P[i + j * m] = z[j];
+      __syncwarp(mask);
     }
-    double* Pg = L + b * Lsize + S.pofs[s];
-    for (int i = 0; i < m * w; ++i) Pg[i] = P[i];
+    // (6) panel out (column-major m x w)
+    double* Pg = L + b * Lsize + M.pofs;
+    for (int e = g; e < m * w; e += TG) Pg[e] = Pn[(e % m) + (e / m) * LD];
+    __syncwarp(mask);
   }
 }
