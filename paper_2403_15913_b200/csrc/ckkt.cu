@@ -271,6 +271,15 @@ __global__ void k_cg_init_scalars(int B, const double* __restrict__ part, double
   done[b] = (t == 0.0) || (skip && skip[b]);
 }
 
+// end of a CG iteration inside the graph loop: continue while some instance is active and the cap
+// is not reached; resets the activity counter for the next iteration
+__global__ void k_cg_cond(int* active, int* loop, int maxit, cudaGraphConditionalHandle h) {
+  const int it = ++(*loop);
+  const unsigned go = (*active > 0 && it < maxit) ? 1u : 0u;
+  *active = 0;
+  cudaGraphSetConditional(h, go);
+}
+
 __global__ void k_copy_neg(int64_t len, const double* __restrict__ a, double sa, double* __restrict__ out) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int b = blockIdx.y;
@@ -512,6 +521,7 @@ struct ckkt_ctx {
   int max_m = 1;
   int ntask = 0, grid_fac = 1, grid_fwd = 1, grid_bwd = 1, grid_ftop = 1, grid_btop = 1;
   int epoch_fac = 0, epoch_fwd = 0, epoch_bwd = 0;
+  int* epoch_dev = nullptr;  // [2] forward / backward sweep epochs, bumped on the device
   Sched Qfac{}, Qfwd{}, Qbwd{};
   int nchunk = 0, nq = 0, nsub = 0;
   int32_t *chunk_ptr = nullptr, *queue = nullptr, *sub_ptr = nullptr, *sub_nodes = nullptr, *topq = nullptr;
@@ -527,6 +537,14 @@ struct ckkt_ctx {
   std::vector<SnMeta> meta_h;
   // phase profiling
   bool profiling = false;
+  // CG loop as a CUDA graph with a device-side WHILE condition (no host round trip per iteration)
+  cudaGraph_t cg_graph = nullptr;
+  cudaGraphExec_t cg_exec = nullptr;
+  cudaGraphConditionalHandle cg_cond = 0;
+  int* cg_loop = nullptr;  // [1] iterations executed by the graph loop
+  int64_t cg_body_launches = 0;
+  bool graph_failed = false;
+  bool graph_pending_loops = false;  // h_pinned_int[4B] holds the loop count of the last graph launch
   std::vector<std::array<cudaEvent_t, 2>> ev_pool;
   std::vector<int> ev_phase;
   size_t ev_used = 0;
@@ -902,6 +920,8 @@ ckkt_status setup_device(ckkt_ctx* c) {
   DALLOC(c->L, (size_t)B * c->Lsize + 4);  // +32 B: 16-byte-rounded L2 prefetches stay in bounds
   DALLOC(c->Ub, (size_t)B * c->Usize);
   DALLOC(c->Vb, (size_t)B * c->Vsize);
+  DALLOC(c->epoch_dev, 2);
+  CK(cudaMemset(c->epoch_dev, 0, 2 * sizeof(int)));
   DALLOC(c->gtv, (size_t)B * std::max<int64_t>(c->g_nnz, 1));
   DALLOC(c->htv, (size_t)B * std::max<int64_t>(c->h_nnz, 1));
   DALLOC(c->notpd, B);
@@ -945,6 +965,7 @@ ckkt_status setup_device(ckkt_ctx* c) {
   DALLOC(c->cg_done, B);
   DALLOC(c->cg_iters, B);
   DALLOC(c->active, 1);
+  DALLOC(c->cg_loop, 1);
   DALLOC(c->accflag, B);
   DALLOC(c->skipflag, B);
   CK(cudaMallocHost(&c->h_pinned_int, sizeof(int) * (5 * B + 16)));
@@ -997,6 +1018,8 @@ void ckkt_destroy(ckkt_ctx* c) {
       cudaEventDestroy(e[0]);
       cudaEventDestroy(e[1]);
     }
+    if (c->cg_exec) cudaGraphExecDestroy(c->cg_exec);
+    if (c->cg_graph) cudaGraphDestroy(c->cg_graph);
     for (void* p : c->owned) cudaFree(p);
     if (c->h_pinned_int) cudaFreeHost(c->h_pinned_int);
     if (c->h_pinned_dbl) cudaFreeHost(c->h_pinned_dbl);
@@ -1200,6 +1223,7 @@ SweepArgs sweep_args(ckkt_ctx* c, const Sched& Q, int epoch, double* x, const in
   a.done_all = Q.done;
   a.B = c->B;
   a.epoch = epoch;
+  a.epoch_ptr = c->epoch_dev + (&Q == &c->Qbwd ? 1 : 0);
   a.L = c->L;
   a.Lsize = c->Lsize;
   a.X = x;
@@ -1216,7 +1240,9 @@ void launch_fwd(ckkt_ctx* c, double* x, const int* skip) {
   prof_begin(c, 2);
   if (c->nsub > 0)
     k_fwd_tiny<<<(c->nsub * c->B * TG + 255) / 256, 256, 0, st>>>(c->S, c->tmeta, c->sub_ptr, c->nsub, c->B, c->L,
-                                                              c->Lsize, x, c->n, c->Vb, c->Vsize, skip);
+                                                              c->Lsize, x, c->n, c->Vb, c->Vsize, skip, c->epoch_dev);
+  else
+    k_epoch_bump<<<1, 1, 0, st>>>(c->epoch_dev);
   DBG_SYNC("k_fwd_tiny");
   ++c->epoch_fwd;
   if (c->nq > 0)
@@ -1264,6 +1290,58 @@ void dot(ckkt_ctx* c, int64_t len, const double* a, const double* b, const int* 
   c->launches++;
 }
 
+// one CG iteration on S_gamma = G K_gamma^{-1} G^T; instances with
+// cg_done set are skipped by every kernel
+void cg_iteration(ckkt_ctx* c) {
+  const int n = c->n, me = c->me, B = c->B;
+  cudaStream_t st = c->stream;
+  const dim3 gn(nblk(n), B), gme(nblk(std::max(me, 1)), B);
+  prof_begin(c, 4);
+  k_gt_spmv<<<gn, TPB, 0, st>>>(n, me, c->gt_ptr, c->gt_e, c->gt_r, c->gtv, c->g_nnz, c->cg_p, 1.0, nullptr, 0.0,
+                                c->vn, c->cg_done);
+  prof_end(c);
+  ksolve(c, c->vn, c->cg_done);
+  prof_begin(c, 4);
+  k_g_spmv<<<gme, TPB, 0, st>>>(me, n, c->g_rowptr, c->g_col2, c->g_val, c->g_nnz, c->vn, 1.0, nullptr, 0.0, c->cg_q,
+                                c->cg_done);
+  dot(c, me, c->cg_p, c->cg_q, c->cg_done);
+  k_cg_alpha<<<nblk(B), TPB, 0, st>>>(B, c->part, c->cg_rr, c->cg_alpha, c->cg_done);
+  k_cg_update_xr<<<gme, TPB, 0, st>>>(me, c->cg_alpha, c->cg_p, c->cg_q, c->cg_x, c->cg_r, c->cg_done);
+  dot(c, me, c->cg_r, c->cg_r, c->cg_done);
+  k_cg_beta<<<nblk(B), TPB, 0, st>>>(B, c->part, c->cg_rr, c->cg_bn, c->opt.cg_rtol, c->cg_beta, c->cg_done,
+                                     c->cg_iters, c->active);
+  k_cg_update_p<<<gme, TPB, 0, st>>>(me, c->cg_beta, c->cg_r, c->cg_p, c->cg_done);
+  c->launches += 7;
+  prof_end(c);
+}
+
+// capture the CG loop once: a conditional WHILE node whose body is one iteration + k_cg_cond
+bool build_cg_graph(ckkt_ctx* c) {
+  cudaStream_t st = c->stream;
+  if (cudaGraphCreate(&c->cg_graph, 0) != cudaSuccess) return false;
+  if (cudaGraphConditionalHandleCreate(&c->cg_cond, c->cg_graph, 1, cudaGraphCondAssignDefault) != cudaSuccess)
+    return false;
+  cudaGraphNodeParams prm = {};
+  prm.type = cudaGraphNodeTypeConditional;
+  prm.conditional.handle = c->cg_cond;
+  prm.conditional.type = cudaGraphCondTypeWhile;
+  prm.conditional.size = 1;
+  cudaGraphNode_t node;
+  if (cudaGraphAddNode(&node, c->cg_graph, nullptr, 0, &prm) != cudaSuccess) return false;
+  cudaGraph_t bodyg = prm.conditional.phGraph_out[0];
+  if (cudaStreamBeginCaptureToGraph(st, bodyg, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed) != cudaSuccess)
+    return false;
+  const int64_t l0 = c->launches;
+  cg_iteration(c);
+  k_cg_cond<<<1, 1, 0, st>>>(c->active, c->cg_loop, c->opt.cg_maxit, c->cg_cond);
+  c->cg_body_launches = c->launches - l0 + 1;
+  c->launches = l0;
+  cudaGraph_t out = nullptr;
+  if (cudaStreamEndCapture(st, &out) != cudaSuccess) return false;
+  if (cudaGraphInstantiate(&c->cg_exec, c->cg_graph, 0) != cudaSuccess) return false;
+  return true;
+}
+
 // One unrefined pass of the strategy for right-hand side (r1 [internal if r1_internal], r2, r3, r4):
 // writes dx (internal), ds, dy, dz.  Returns the total CG iterations (host copy, per instance) via c->cg_iters.
 ckkt_status solve_pass(ckkt_ctx* c, const double* r1, int r1_internal, const double* r2, const double* r3,
@@ -1296,30 +1374,26 @@ ckkt_status solve_pass(ckkt_ctx* c, const double* r1, int r1_internal, const dou
     k_cg_init_scalars<<<nblk(B), TPB, 0, st>>>(B, c->part, c->cg_rr, c->cg_bn, c->cg_done, c->cg_iters, skip);
     c->launches += 4;
     prof_end(c);
-    for (int it = 0; it < c->opt.cg_maxit; ++it) {
-      // q = G K^{-1} G^T p
-      prof_begin(c, 4);
-      k_gt_spmv<<<gn, TPB, 0, st>>>(n, me, c->gt_ptr, c->gt_e, c->gt_r, c->gtv, c->g_nnz, c->cg_p, 1.0, nullptr,
-                                    0.0, c->vn, c->cg_done);
-      prof_end(c);
-      ksolve(c, c->vn, c->cg_done);
-      prof_begin(c, 4);
-      k_g_spmv<<<gme, TPB, 0, st>>>(me, n, c->g_rowptr, c->g_col2, c->g_val, c->g_nnz, c->vn, 1.0, nullptr, 0.0,
-                                    c->cg_q, c->cg_done);
-      dot(c, me, c->cg_p, c->cg_q, c->cg_done);
-      k_cg_alpha<<<nblk(B), TPB, 0, st>>>(B, c->part, c->cg_rr, c->cg_alpha, c->cg_done);
-      k_cg_update_xr<<<gme, TPB, 0, st>>>(me, c->cg_alpha, c->cg_p, c->cg_q, c->cg_x, c->cg_r, c->cg_done);
-      dot(c, me, c->cg_r, c->cg_r, c->cg_done);
-      cudaMemsetAsync(c->active, 0, sizeof(int), st);
-      k_cg_beta<<<nblk(B), TPB, 0, st>>>(B, c->part, c->cg_rr, c->cg_bn, c->opt.cg_rtol, c->cg_beta, c->cg_done,
-                                         c->cg_iters, c->active);
-      k_cg_update_p<<<gme, TPB, 0, st>>>(me, c->cg_beta, c->cg_r, c->cg_p, c->cg_done);
-      c->launches += 7;
-      prof_end(c);
-      int* h_active = c->h_pinned_int + 4 * B;
-      CK(cudaMemcpyAsync(h_active, c->active, sizeof(int), cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      if (*h_active == 0) break;
+    const bool use_graph = !c->profiling && !c->graph_failed && !sync_debug() && !getenv("CKKT_NO_GRAPH");
+    if (use_graph && !c->cg_exec && !build_cg_graph(c)) {
+      c->graph_failed = true;  // fall back to the host-driven loop
+      cudaGetLastError();
+    }
+    if (use_graph && c->cg_exec) {
+      CK(cudaMemsetAsync(c->active, 0, sizeof(int), st));
+      CK(cudaMemsetAsync(c->cg_loop, 0, sizeof(int), st));
+      CK(cudaGraphLaunch(c->cg_exec, st));
+      CK(cudaMemcpyAsync(c->h_pinned_int + 4 * B, c->cg_loop, sizeof(int), cudaMemcpyDeviceToHost, st));
+      c->graph_pending_loops = true;
+    } else {
+      for (int it = 0; it < c->opt.cg_maxit; ++it) {
+        CK(cudaMemsetAsync(c->active, 0, sizeof(int), st));
+        cg_iteration(c);
+        int* h_active = c->h_pinned_int + 4 * B;
+        CK(cudaMemcpyAsync(h_active, c->active, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (*h_active == 0) break;
+      }
     }
     // dy = x ; dx = K^{-1}(-r_gamma - G^T dy)
     prof_begin(c, 4);
@@ -1333,6 +1407,10 @@ ckkt_status solve_pass(ckkt_ctx* c, const double* r1, int r1_internal, const dou
     CK(cudaMemcpyAsync(h_iters, c->cg_iters, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     for (int b = 0; b < B; ++b) kcg[b] = h_iters[b];
+    if (c->graph_pending_loops) {  // kernels launched by the graph loop (telemetry)
+      c->launches += (int64_t)c->h_pinned_int[4 * B] * c->cg_body_launches;
+      c->graph_pending_loops = false;
+    }
   } else {
     k_copy_neg<<<gn, TPB, 0, st>>>(n, c->rg, -1.0, dx);
     c->launches++;
@@ -1631,6 +1709,7 @@ extern "C" int ckkt_debug_trace_bwd(ckkt_ctx* c, unsigned long long* host_ts) {
     cudaMemcpyToSymbol(g_debug_ph, &dph, sizeof(dph));
     ckkt_refactor(c, c->w_val, c->g_val, c->h_val, c->sigma, c->d_s, c->delta, nullptr, nullptr);
   } else {
+    launch_fwd(c, c->tn, nullptr);  // (the forward sweep's first launch bumps the sweep epochs)
     launch_bwd(c, c->tn, nullptr);
   }
   cudaStreamSynchronize(c->stream);

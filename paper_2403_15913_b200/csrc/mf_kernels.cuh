@@ -492,7 +492,8 @@ struct SweepArgs {
   int ns;                    // done-flag stride
   int* ctr;                  // [4]: warp tickets (2 epoch slots), CTA tickets (2 epoch slots)
   int* done_all;
-  int B, epoch;
+  int B, epoch;              // epoch is re-read from *epoch_ptr at kernel start (device-side counter)
+  const int* epoch_ptr;
   const double* L;
   int64_t Lsize;
   double* X;
@@ -616,6 +617,7 @@ __device__ __forceinline__ void fwd_cta_step(const SymDev& S, const SweepArgs& A
 }
 
 __global__ void __launch_bounds__(32 * SOLVE_WARPS, SOLVE_MINB) k_fwd_persist(SymDev S, SweepArgs A) {
+  A.epoch = *A.epoch_ptr;  // bumped by the sweep's first launch (CUDA-graph safe)
   extern __shared__ double smem[];
   __shared__ int tk_sh[SOLVE_WARPS + 1];
   __shared__ ChMeta cmeta_all[SOLVE_WARPS][32];
@@ -733,6 +735,7 @@ __device__ __forceinline__ void bwd_cta_step(const SymDev& S, const SweepArgs& A
 }
 
 __global__ void __launch_bounds__(32 * SOLVE_WARPS, SOLVE_MINB) k_bwd_persist(SymDev S, SweepArgs A) {
+  A.epoch = *A.epoch_ptr;  // bumped by the sweep's first launch (CUDA-graph safe)
   extern __shared__ double smem[];
   __shared__ int tk_sh[SOLVE_WARPS + 1];
   __shared__ SnMeta msh_all[SOLVE_WARPS][16];
@@ -867,6 +870,7 @@ __device__ __forceinline__ void top_reserve_next(const SweepArgs& A, int* ctr, T
 }
 
 __global__ void __launch_bounds__(TOP_THREADS, TOP_MINB) k_fwd_top(SymDev S, SweepArgs A) {
+  A.epoch = *A.epoch_ptr;  // bumped by the sweep's first launch (CUDA-graph safe)
   extern __shared__ __align__(16) double smem[];
   __shared__ TopShared sh;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -988,6 +992,7 @@ __global__ void __launch_bounds__(TOP_THREADS, TOP_MINB) k_fwd_top(SymDev S, Swe
 }
 
 __global__ void __launch_bounds__(TOP_THREADS, TOP_MINB) k_bwd_top(SymDev S, SweepArgs A) {
+  A.epoch = *A.epoch_ptr;  // bumped by the sweep's first launch (CUDA-graph safe)
   extern __shared__ __align__(16) double smem[];
   __shared__ TopShared sh;
   __shared__ double red[TOP_WARPS][TOP_CPW * 33 + 32];
@@ -1126,8 +1131,12 @@ static_assert(TINY_M <= 32 && 32 % TG == 0, "tiny sweep layout");
 __global__ void __launch_bounds__(256)
     k_fwd_tiny(SymDev S, const SnMeta* __restrict__ tmeta, const int32_t* __restrict__ sub_ptr, int nsub, int B,
                const double* __restrict__ L, int64_t Lsize, double* X, int n, double* Vb, int64_t Vsize,
-               const int* __restrict__ skip) {
+               const int* __restrict__ skip, int* epoch_dev) {
   __shared__ double vsh_all[256 / TG][TINY_M];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // new sweep epochs (forward and the backward that follows)
+    epoch_dev[0] += 1;
+    epoch_dev[1] += 1;
+  }
   const int gid = (blockIdx.x * blockDim.x + threadIdx.x) / TG, g = threadIdx.x % TG;
   if (gid >= nsub * B) return;  // group-uniform
   const unsigned mask = (TG == 32 ? 0xFFFFFFFFu : ((1u << TG) - 1u)) << ((threadIdx.x & 31) & ~(TG - 1));
@@ -1241,6 +1250,11 @@ __global__ void __launch_bounds__(256)
 // Same arithmetic as the big fronts: assemble A + children's panel parts, Cholesky of
 // the w columns, U_s = -L21 L21^T plus the children's trailing parts, L11 <- L11^{-1}.
 constexpr int FT_THREADS = 256;
+
+__global__ void k_epoch_bump(int* epoch_dev) {  // sweeps without tiny subtrees
+  epoch_dev[0] += 1;
+  epoch_dev[1] += 1;
+}
 __global__ void __launch_bounds__(FT_THREADS)
     k_factor_tiny(SymDev S, const SnMeta* __restrict__ tmeta, const int32_t* __restrict__ sub_ptr, int nsub, int B,
                   double* L, int64_t Lsize, double* Ub, int64_t Usize, const double* __restrict__ Kval, int64_t nnzk,

@@ -47,4 +47,5 @@ print('height: count traced, tick min, wake min/max, end max, proc mean, bytes M
 for lv in range(h.max() + 1):
     ss = done & (h == lv)
     if ss.any():
-        print(f"  h={lv:2d} n={ss.sum():7d} tick [{tick[ss].min():6.0f}] wake [{wake[ss].min():6.0f},{wake[ss].max():6.0f}] end {end[ss].max():6.0f} proc {proc[ss].mean():5.1f} MB {pw[ss].sum()*8/1e6:7.1f}")
+        st = ss & (kind == 1)
+        print(f"  h={lv:2d} n={ss.sum():7d} top {st.sum():6d} tick [{tick[ss].min():6.0f}] wake [{wake[ss].min():6.0f},{wake[ss].max():6.0f}] end {end[ss].max():6.0f} proc {proc[ss].mean():5.1f} MB {pw[ss].sum()*8/1e6:7.1f}" + (f" top: start [{tick[st].min():5.0f},{tick[st].max():5.0f}] end [{end[st].min():5.0f},{end[st].max():5.0f}] wait {(wake-tick)[st].mean():4.1f} proc {proc[st].mean():4.1f}" if st.any() else ""))
