@@ -721,9 +721,9 @@ ckkt_status setup_device(ckkt_ctx* c) {
     c->Qfwd = Sched{c->ntask, d_tsn, d_tbig, dfwd, cfwd};
     c->Qbwd = Sched{c->ntask, d_tsn, d_tbig, dbwd, cbwd};
     c->fac_smem = std::max<int64_t>(c->big_smem, 8 * SMALL_WARPS * SMALL_PANEL);
-    c->sol_smem = 8 * ((int64_t)SOLVE_WARPS * (c->max_m + 64 + 16 * 33) + c->max_m + 128) +
-                  4 * (int64_t)SOLVE_WARPS * c->max_m;  // + per-warp row indices (backward)
-    c->fwd_smem = 8 * ((int64_t)SOLVE_WARPS * (c->max_m + 64) + c->max_m + 64);
+    c->sol_smem = 8 * ((int64_t)SOLVE_WORKERS * (c->max_m + 64 + RED_SZ)) +
+                  4 * (int64_t)SOLVE_WORKERS * c->max_m;  // + per-worker row indices (backward)
+    c->fwd_smem = 8 * ((int64_t)SOLVE_WORKERS * (c->max_m + 64));
     if (c->fac_smem > 227 * 1024 || c->sol_smem > 227 * 1024) return CKKT_INVALID_ARG;
     CK(cudaFuncSetAttribute(k_factor_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->fac_smem));
     CK(cudaFuncSetAttribute(k_fwd_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->fwd_smem));
@@ -864,7 +864,7 @@ ckkt_status setup_device(ckkt_ctx* c) {
         c->qmeta = upload(qm, o, by);
         if (!c->qmeta && !q.empty()) return CKKT_OUT_OF_MEMORY;
       }
-      const int64_t warps = (int64_t)c->grid_fwd * SOLVE_WARPS;
+      const int64_t warps = (int64_t)c->grid_fwd * SOLVE_WORKERS;  // bottom-set workers
       std::vector<int32_t> cp{0};
       for (int l = 0; l < A.nlevels; ++l) {
         const int64_t K = lp[l + 1] - lp[l];

@@ -368,10 +368,25 @@ constexpr int SOLVE_WARPS = 8;
 #define CKKT_SOLVE_MINB 3
 #endif
 constexpr int SOLVE_MINB = CKKT_SOLVE_MINB;  // resident CTAs per SM the register budget is sized for
-constexpr int TOP_PANEL = 4096;  // panels above this (doubles) and their ancestors are swept by a whole CTA
+constexpr int TOP_PANEL = 4096;  // panels above this (doubles) and their ancestors go to the top set
+// Bottom-set sweeps run one supernode per WORKER of LW lanes (a warp, or a half warp: two
+// independent supernode chains interleaved in one warp hide more memory latency per SM).
+#ifndef CKKT_LW
+#define CKKT_LW 32
+#endif
+constexpr int LW = CKKT_LW;
+constexpr int SOLVE_WORKERS = 32 * SOLVE_WARPS / LW;  // workers per CTA
+constexpr int RED_LD = LW + 1;                         // column stride of the per-worker reduction scratch
+constexpr int RED_SZ = 16 * RED_LD;                    // doubles of it (16 columns per batch)
+static_assert(LW == 32 || LW == 16, "worker width");
+
+__device__ __forceinline__ unsigned worker_mask() {
+  return LW == 32 ? 0xFFFFFFFFu : (0xFFFFu << (threadIdx.x & 16));
+}
+__device__ __forceinline__ void wsync() { __syncwarp(worker_mask()); }
 
 // out[i] = init[i] + sgn * sum_{k<ncols} A[i + k*ld] * xv[k],  i < nrows   (lanes over rows)
-// RB row blocks of 32 per pass and CB = 16/RB columns per batch: 16 independent loads per lane in flight.
+// RB row blocks of LW per pass and CB = 16/RB columns per batch: 16 independent loads per lane in flight.
 template <int RB>
 __device__ __forceinline__ void warp_gemv_rb(const double* __restrict__ A, int ld, int r0, int nrows, int ncols,
                                              const double* xv, const double* init, double sgn, double* out,
@@ -380,7 +395,7 @@ __device__ __forceinline__ void warp_gemv_rb(const double* __restrict__ A, int l
   double acc[RB];
 #pragma unroll
   for (int r = 0; r < RB; ++r) {
-    const int i = r0 + r * 32 + lane;
+    const int i = r0 + r * LW + lane;
     acc[r] = (init && i < nrows) ? init[i] : 0.0;
   }
   for (int k0 = 0; k0 < ncols; k0 += CB) {
@@ -389,7 +404,7 @@ __device__ __forceinline__ void warp_gemv_rb(const double* __restrict__ A, int l
     for (int kk = 0; kk < CB; ++kk)
 #pragma unroll
       for (int r = 0; r < RB; ++r) {
-        const int i = r0 + r * 32 + lane, k = k0 + kk;
+        const int i = r0 + r * LW + lane, k = k0 + kk;
         a[kk][r] = (k < ncols && i < nrows) ? A[i + (int64_t)k * ld] : 0.0;
       }
 #pragma unroll
@@ -401,7 +416,7 @@ __device__ __forceinline__ void warp_gemv_rb(const double* __restrict__ A, int l
   }
 #pragma unroll
   for (int r = 0; r < RB; ++r) {
-    const int i = r0 + r * 32 + lane;
+    const int i = r0 + r * LW + lane;
     if (i < nrows) out[i] = acc[r];
   }
 }
@@ -409,10 +424,10 @@ __device__ __forceinline__ void warp_gemv_rb(const double* __restrict__ A, int l
 __device__ __forceinline__ void warp_gemv(const double* __restrict__ A, int ld, int nrows, int ncols,
                                           const double* xv, const double* init, double sgn, double* out, int lane) {
   int r0 = 0;
-  for (; nrows - r0 > 96; r0 += 128) warp_gemv_rb<4>(A, ld, r0, nrows, ncols, xv, init, sgn, out, lane);
+  for (; nrows - r0 > 3 * LW; r0 += 4 * LW) warp_gemv_rb<4>(A, ld, r0, nrows, ncols, xv, init, sgn, out, lane);
   const int rem = nrows - r0;
-  if (rem > 64) warp_gemv_rb<4>(A, ld, r0, nrows, ncols, xv, init, sgn, out, lane);
-  else if (rem > 32) warp_gemv_rb<2>(A, ld, r0, nrows, ncols, xv, init, sgn, out, lane);
+  if (rem > 2 * LW) warp_gemv_rb<4>(A, ld, r0, nrows, ncols, xv, init, sgn, out, lane);
+  else if (rem > LW) warp_gemv_rb<2>(A, ld, r0, nrows, ncols, xv, init, sgn, out, lane);
   else if (rem > 0) warp_gemv_rb<1>(A, ld, r0, nrows, ncols, xv, init, sgn, out, lane);
 }
 
@@ -429,11 +444,11 @@ __device__ __forceinline__ void warp_coldot_rb(const double* __restrict__ A, int
     double acc[CB];
 #pragma unroll
     for (int cc = 0; cc < CB; ++cc) acc[cc] = 0.0;
-    for (int i0 = 0; i0 < nrows; i0 += 32 * RB) {
+    for (int i0 = 0; i0 < nrows; i0 += LW * RB) {
       double a[RB][CB], xr[RB];
 #pragma unroll
       for (int r = 0; r < RB; ++r) {
-        const int i = i0 + r * 32 + lane;
+        const int i = i0 + r * LW + lane;
         xr[r] = (i < nrows) ? xv[i] : 0.0;
 #pragma unroll
         for (int cc = 0; cc < CB; ++cc)
@@ -445,40 +460,38 @@ __device__ __forceinline__ void warp_coldot_rb(const double* __restrict__ A, int
         for (int cc = 0; cc < CB; ++cc) acc[cc] += a[r][cc] * xr[r];
     }
 #pragma unroll
-    for (int cc = 0; cc < CB; ++cc) red[cc * 33 + lane] = acc[cc];
-    __syncwarp();
+    for (int cc = 0; cc < CB; ++cc) red[cc * RED_LD + lane] = acc[cc];
+    wsync();
     if (lane < CB && c0 + lane < ncols) {
       double v = 0.0;
 #pragma unroll 8
-      for (int l = 0; l < 32; ++l) v += red[lane * 33 + l];
+      for (int l = 0; l < LW; ++l) v += red[lane * RED_LD + l];
       out[c0 + lane] = (init ? init[c0 + lane] : 0.0) + sgn * v;
     }
-    __syncwarp();
+    wsync();
   }
 }
 
 __device__ __forceinline__ void warp_coldot(const double* __restrict__ A, int ld, int nrows, int ncols,
                                             const double* xv, const double* init, double sgn, double* out,
-                                            int lane, double* red /* [16 * 33] shared */) {
-  if (nrows > 64) warp_coldot_rb<4>(A, ld, nrows, ncols, xv, init, sgn, out, lane, red);
-  else if (nrows > 32) warp_coldot_rb<2>(A, ld, nrows, ncols, xv, init, sgn, out, lane, red);
+                                            int lane, double* red /* [RED_SZ] shared */) {
+  if (nrows > 2 * LW) warp_coldot_rb<4>(A, ld, nrows, ncols, xv, init, sgn, out, lane, red);
+  else if (nrows > LW) warp_coldot_rb<2>(A, ld, nrows, ncols, xv, init, sgn, out, lane, red);
   else warp_coldot_rb<1>(A, ld, nrows, ncols, xv, init, sgn, out, lane, red);
 }
 
 __device__ __forceinline__ int warp_ticket(int* ctr_slot, int lane, volatile int* sh) {
-  __syncwarp();
+  wsync();
   if (lane == 0) *sh = atomicAdd(ctr_slot, 1);
-  __syncwarp();
+  wsync();
   return *sh;
 }
 
 // ---------------------------------------------------------------------------------------------
-// Sweeps are two-mode persistent kernels.  The "top" set (large supernodes and all their
-// ancestors; ancestor-closed) is processed one supernode per CTA (8 warps split the rows /
-// columns), everything else one supernode per warp.  Forward: warp mode over the bottom queue,
-// then CTA mode over the top queue; backward: CTA mode first, then warp mode.  Bottom tasks never
-// depend on top tasks in the forward sweep (and vice versa in the backward sweep), so each CTA
-// switches mode exactly once.
+// Bottom-set sweeps: persistent kernels, one supernode per worker, workers take chunks of the
+// level-ordered bottom queue from an atomic ticket counter.  The top set (large panels and their
+// ancestors; ancestor-closed) runs in k_fwd_top / k_bwd_top: forward after this kernel, backward
+// before it (bottom tasks never depend on top tasks in the forward sweep, and vice versa).
 // ---------------------------------------------------------------------------------------------
 struct SweepArgs {
   const int32_t* queue;      // bottom supernodes, level order
@@ -490,7 +503,7 @@ struct SweepArgs {
   int ntop;
   int topbuf;                // doubles of the top kernels' shared-memory panel buffer
   int ns;                    // done-flag stride
-  int* ctr;                  // [4]: warp tickets (2 epoch slots), CTA tickets (2 epoch slots)
+  int* ctr;                  // [4]: worker tickets (2 epoch slots), top-kernel tickets (2 epoch slots)
   int* done_all;
   int B, epoch;              // epoch is re-read from *epoch_ptr at kernel start (device-side counter)
   const int* epoch_ptr;
@@ -504,51 +517,42 @@ struct SweepArgs {
   const int* skip;
 };
 
-__device__ __forceinline__ int cta_ticket(int* ctr_slot, volatile int* sh) {
-  __syncthreads();
-  if (threadIdx.x == 0) *sh = atomicAdd(ctr_slot, 1);
-  __syncthreads();
-  return *sh;
-}
-
 // v[rel_c] += u_c for the children c of M (extend-add of the update vectors), children in
 // a fixed order (deterministic; rows inside one child are distinct so lanes never collide)
 __device__ __forceinline__ void warp_gather_children(const SymDev& S, const SweepArgs& A, const SnMeta& M, int b,
                                                      int lane, double* v, ChMeta* cmeta, int* done) {
   const double* Vb = A.Vb + b * A.Vsize;
-  for (int cb = M.ch0; cb < M.ch1; cb += 32) {
-    const int nc = min(32, M.ch1 - cb);
+  for (int cb = M.ch0; cb < M.ch1; cb += LW) {
+    const int nc = min(LW, M.ch1 - cb);
     if (lane < nc) {
       const ChMeta cm = S.chmeta[cb + lane];
       cmeta[lane] = cm;
       if (!cm.tiny) wait_epoch(done + cm.c, A.epoch);
     }
-    __syncwarp();
+    wsync();
     for (int k = 0; k < nc; ++k) {
       const ChMeta cm = cmeta[k];
       const double* uc = Vb + cm.vofs;
       const int32_t* rel = S.relmap + cm.relofs;
-      for (int i = lane; i < cm.mc; i += 32) v[__ldg(rel + i)] += __ldcg(uc + i);
-      __syncwarp();
+      for (int i = lane; i < cm.mc; i += LW) v[__ldg(rel + i)] += __ldcg(uc + i);
+      wsync();
     }
   }
 }
 
-// forward step of supernode s by one warp (v, y: per-warp shared scratch)
+// forward step of supernode s by one worker (v, y: per-worker shared scratch)
 __device__ __forceinline__ void fwd_warp_step(const SymDev& S, const SweepArgs& A, const SnMeta& M, int s, int b,
                                               int lane, double* v, double* y, ChMeta* cmeta, int* done) {
   double* x = A.X + (int64_t)b * A.n;
   const int f = M.f, w = M.w, m = M.m, mu = m - w;
   const double* P = A.L + b * A.Lsize + M.pofs;
-#ifndef CKKT_CHUNK_PREFETCH
   if (lane == 0) prefetch_l2(P, 8ll * m * w);  // the panel streams into L2 while the children are gathered
-#endif
   const unsigned long long t0 = g_debug_ts ? gtimer() : 0ull;
-  for (int i = lane; i < m; i += 32) v[i] = (i < w) ? x[f + i] : 0.0;
+  for (int i = lane; i < m; i += LW) v[i] = (i < w) ? x[f + i] : 0.0;
   warp_gather_children(S, A, M, b, lane, v, cmeta, done);
   warp_gemv(P, m, w, w, v, nullptr, 1.0, y, lane);  // y = Z v[0:w]  (Z strict upper part is zero)
-  __syncwarp();
-  for (int i = lane; i < w; i += 32) x[f + i] = y[i];
+  wsync();
+  for (int i = lane; i < w; i += LW) x[f + i] = y[i];
   warp_gemv(P + w, m, mu, w, y, v + w, -1.0, A.Vb + b * A.Vsize + M.vofs, lane);
   if (g_debug_ts && lane == 0 && b == 0) {
     g_debug_ts[4 * s] = t0;
@@ -558,82 +562,38 @@ __device__ __forceinline__ void fwd_warp_step(const SymDev& S, const SweepArgs& 
   }
 }
 
-// stage the metadata of queue entries [q0, q0 + n) (n <= 16) into shared memory and start the
-// L2 prefetch of their panels (and, backward, of their row index lists)
+// stage the metadata of queue entries [q0, q0 + n) (n <= 16) into shared memory (and, backward,
+// start the L2 prefetch of their row index lists)
 __device__ __forceinline__ void warp_stage_chunk(const SymDev& S, const SweepArgs& A, int q0, int n, int b, int lane,
                                                  SnMeta* msh, bool rows) {
   const long long* src = reinterpret_cast<const long long*>(A.qmeta + q0);
   long long* dst = reinterpret_cast<long long*>(msh);
   constexpr int WPM = sizeof(SnMeta) / 8;
-  for (int k = lane; k < n * WPM; k += 32) dst[k] = __ldg(src + k);
-  __syncwarp();
-  if (lane < n) {
+  for (int k = lane; k < n * WPM; k += LW) dst[k] = __ldg(src + k);
+  wsync();
+  if (lane < n && rows) {
     const SnMeta& M = msh[lane];
-#ifdef CKKT_CHUNK_PREFETCH
-    prefetch_l2(A.L + b * A.Lsize + M.pofs, 8ll * M.m * M.w);
-#endif
-    if (rows) prefetch_l2(S.srows + M.r0 + M.w, 4ll * (M.m - M.w));
-  }
-}
-
-// forward step of a top supernode by the whole CTA (v, y: CTA shared scratch)
-__device__ __forceinline__ void fwd_cta_step(const SymDev& S, const SweepArgs& A, int s, int b, double* v, double* y,
-                                             ChMeta* cmeta, int* done) {
-  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
-  const SnMeta M = S.meta[s];
-  double* x = A.X + (int64_t)b * A.n;
-  const int f = M.f, w = M.w, m = M.m, mu = m - w;
-  const double* P = A.L + b * A.Lsize + M.pofs;
-  if (tid == 0) prefetch_l2(P, 8ll * m * w);
-  const unsigned long long t0 = g_debug_ts ? gtimer() : 0ull;
-  for (int i = tid; i < m; i += nt) v[i] = (i < w) ? x[f + i] : 0.0;
-  for (int cb = M.ch0; cb < M.ch1; cb += 32) {
-    const int nc = min(32, M.ch1 - cb);
-    if (warp == 0 && lane < nc) {
-      const ChMeta cm = S.chmeta[cb + lane];
-      cmeta[lane] = cm;
-      if (!cm.tiny) wait_epoch(done + cm.c, A.epoch);
-    }
-    __syncthreads();
-    for (int k = 0; k < nc; ++k) {
-      const ChMeta cm = cmeta[k];
-      const double* uc = A.Vb + b * A.Vsize + cm.vofs;
-      const int32_t* rel = S.relmap + cm.relofs;
-      for (int i = tid; i < cm.mc; i += nt) v[__ldg(rel + i)] += __ldcg(uc + i);
-      __syncthreads();
-    }
-  }
-  for (int r0 = warp * 32; r0 < w; r0 += nwarp * 32) warp_gemv_rb<1>(P, m, r0, w, w, v, nullptr, 1.0, y, lane);
-  __syncthreads();
-  for (int i = tid; i < w; i += nt) x[f + i] = y[i];
-  double* us = A.Vb + b * A.Vsize + M.vofs;
-  for (int r0 = warp * 32; r0 < mu; r0 += nwarp * 32) warp_gemv_rb<1>(P + w, m, r0, mu, w, y, v + w, -1.0, us, lane);
-  if (g_debug_ts && tid == 0 && b == 0) {
-    g_debug_ts[4 * s] = t0;
-    g_debug_ts[4 * s + 1] = t0;
-    g_debug_ts[4 * s + 2] = gtimer();
-    g_debug_ts[4 * s + 3] = 1;
+    prefetch_l2(S.srows + M.r0 + M.w, 4ll * (M.m - M.w));
   }
 }
 
 __global__ void __launch_bounds__(32 * SOLVE_WARPS, SOLVE_MINB) k_fwd_persist(SymDev S, SweepArgs A) {
   A.epoch = *A.epoch_ptr;  // bumped by the sweep's first launch (CUDA-graph safe)
   extern __shared__ double smem[];
-  __shared__ int tk_sh[SOLVE_WARPS + 1];
-  __shared__ ChMeta cmeta_all[SOLVE_WARPS][32];
-  __shared__ SnMeta msh_all[SOLVE_WARPS][16];
+  __shared__ int tk_sh[SOLVE_WORKERS];
+  __shared__ ChMeta cmeta_all[SOLVE_WORKERS][LW];
+  __shared__ SnMeta msh_all[SOLVE_WORKERS][16];
   if (blockIdx.x == 0 && threadIdx.x == 0) {  // slots of the next launch
     A.ctr[(A.epoch + 1) & 1] = 0;
     A.ctr[2 + ((A.epoch + 1) & 1)] = 0;
   }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double* v = smem + (size_t)warp * (A.max_m + 64);
+  const int lane = threadIdx.x % LW, wk = threadIdx.x / LW;
+  double* v = smem + (size_t)wk * (A.max_m + 64);
   double* y = v + A.max_m;
-  ChMeta* cmeta = cmeta_all[warp];
-  SnMeta* msh = msh_all[warp];
-  // warp mode: bottom queue in chunks
+  ChMeta* cmeta = cmeta_all[wk];
+  SnMeta* msh = msh_all[wk];
   for (;;) {
-    const int t = warp_ticket(&A.ctr[A.epoch & 1], lane, &tk_sh[warp]);
+    const int t = warp_ticket(&A.ctr[A.epoch & 1], lane, &tk_sh[wk]);
     if (t >= A.nchunk * A.B) break;
     const int ch = t / A.B, b = t % A.B;
     int* done = A.done_all + (int64_t)b * A.ns;
@@ -644,50 +604,35 @@ __global__ void __launch_bounds__(32 * SOLVE_WARPS, SOLVE_MINB) k_fwd_persist(Sy
       const int s = sk ? A.queue[q0 + j] : msh[j].pad1;
       if (!sk) {
         fwd_warp_step(S, A, msh[j], s, b, lane, v, y, cmeta, done);
-        __syncwarp();
+        wsync();
       }
       if (lane == 0) st_release(done + s, A.epoch);
     }
-    __syncwarp();
-  }
-  // CTA mode: top queue
-  double* vc = smem + (size_t)SOLVE_WARPS * (A.max_m + 64);
-  for (; A.ntop > 0;) {  // (ntop = 0 when the top set runs in k_fwd_top: its ticket slot stays untouched)
-    const int t = cta_ticket(&A.ctr[2 + (A.epoch & 1)], &tk_sh[SOLVE_WARPS]);
-    if (t >= A.ntop * A.B) break;
-    const int s = A.top[t / A.B], b = t % A.B;
-    int* done = A.done_all + (int64_t)b * A.ns;
-    if (!(A.skip && A.skip[b])) {
-      fwd_cta_step(S, A, s, b, vc, vc + A.max_m, cmeta_all[0], done);
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) st_release(done + s, A.epoch);
+    wsync();
   }
 }
 
-// backward step of supernode s by one warp: x_s = Z^T (y_s - L21^T x_R)
+// backward step of supernode s by one worker: x_s = Z^T (y_s - L21^T x_R)
 __device__ __forceinline__ void bwd_warp_step(const SymDev& S, const SweepArgs& A, const SnMeta& M, int s, int b,
                                               int lane, double* xr, double* tv, double* red, int* ridx, int* done) {
   const int p = M.pad0;
   double* x = A.X + (int64_t)b * A.n;
   const int f = M.f, w = M.w, m = M.m, mu = m - w;
   const double* P = A.L + b * A.Lsize + M.pofs;
-#ifndef CKKT_CHUNK_PREFETCH
   if (lane == 0) prefetch_l2(P, 8ll * m * w);  // independent of the parent: overlap with the wait
-#endif
-  for (int i = lane; i < w; i += 32) tv[i] = x[f + i];
-  for (int i = lane; i < mu; i += 32) ridx[i] = __ldg(S.srows + M.r0 + w + i);
+  for (int i = lane; i < w; i += LW) tv[i] = x[f + i];
+  for (int i = lane; i < mu; i += LW) ridx[i] = __ldg(S.srows + M.r0 + w + i);
   const unsigned long long t0 = g_debug_ts ? gtimer() : 0ull;
   if (p >= 0) wait_epoch(done + p, A.epoch);  // all lanes: uniform control flow
-  __syncwarp();
+  wsync();
   const unsigned long long t1 = g_debug_ts ? gtimer() : 0ull;
-  for (int i = lane; i < mu; i += 32) xr[i] = __ldcg(x + ridx[i]);
-  __syncwarp();
+  for (int i = lane; i < mu; i += LW) xr[i] = __ldcg(x + ridx[i]);
+  wsync();
   warp_coldot(P + w, m, mu, w, xr, tv, -1.0, tv, lane, red);  // t = y - L21^T x_R
-  __syncwarp();
+  wsync();
   warp_coldot(P, m, w, w, tv, nullptr, 1.0, xr, lane, red);   // x_s = Z^T t  (xr reused as output)
-  __syncwarp();
-  for (int i = lane; i < w; i += 32) x[f + i] = xr[i];
+  wsync();
+  for (int i = lane; i < w; i += LW) x[f + i] = xr[i];
   if (g_debug_ts && lane == 0 && b == 0) {
     g_debug_ts[4 * s] = t0;
     g_debug_ts[4 * s + 1] = t1;
@@ -696,92 +641,39 @@ __device__ __forceinline__ void bwd_warp_step(const SymDev& S, const SweepArgs& 
   }
 }
 
-// backward step of a top supernode by the whole CTA: warps split the columns
-__device__ __forceinline__ void bwd_cta_step(const SymDev& S, const SweepArgs& A, int s, int b, double* xr, double* tv,
-                                             double* xo, double* red_warp, int* done) {
-  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
-  const SnMeta M = S.meta[s];
-  const int p = S.sparent[s];
-  double* x = A.X + (int64_t)b * A.n;
-  const int f = M.f, w = M.w, m = M.m, mu = m - w;
-  const double* P = A.L + b * A.Lsize + M.pofs;
-  if (tid == 0) prefetch_l2(P, 8ll * m * w);
-  for (int i = tid; i < w; i += nt) tv[i] = x[f + i];
-  int ri[4];  // row indices of this thread (mu <= 4 * blockDim), loaded before the wait
-#pragma unroll
-  for (int k = 0; k < 4; ++k) ri[k] = (tid + k * nt < mu) ? __ldg(S.srows + M.r0 + w + tid + k * nt) : 0;
-  const unsigned long long t0 = g_debug_ts ? gtimer() : 0ull;
-  if (tid == 0 && p >= 0) wait_epoch(done + p, A.epoch);
-  __syncthreads();
-  const unsigned long long t1 = g_debug_ts ? gtimer() : 0ull;
-#pragma unroll
-  for (int k = 0; k < 4; ++k)
-    if (tid + k * nt < mu) xr[tid + k * nt] = __ldcg(x + ri[k]);
-  for (int i = tid + 4 * nt; i < mu; i += nt) xr[i] = __ldcg(x + __ldg(S.srows + M.r0 + w + i));
-  __syncthreads();
-  const int cpw = (w + nwarp - 1) / nwarp;  // columns per warp
-  const int c0 = warp * cpw, nc = max(0, min(cpw, w - c0));
-  if (nc > 0) warp_coldot(P + w + (int64_t)c0 * m, m, mu, nc, xr, tv + c0, -1.0, tv + c0, lane, red_warp);
-  __syncthreads();
-  if (nc > 0) warp_coldot(P + (int64_t)c0 * m, m, w, nc, tv, nullptr, 1.0, xo + c0, lane, red_warp);
-  __syncthreads();
-  for (int i = tid; i < w; i += nt) x[f + i] = xo[i];
-  if (g_debug_ts && tid == 0 && b == 0) {
-    g_debug_ts[4 * s] = t0;
-    g_debug_ts[4 * s + 1] = t1;
-    g_debug_ts[4 * s + 2] = gtimer();
-    g_debug_ts[4 * s + 3] = 1;
-  }
-}
-
 __global__ void __launch_bounds__(32 * SOLVE_WARPS, SOLVE_MINB) k_bwd_persist(SymDev S, SweepArgs A) {
   A.epoch = *A.epoch_ptr;  // bumped by the sweep's first launch (CUDA-graph safe)
   extern __shared__ double smem[];
-  __shared__ int tk_sh[SOLVE_WARPS + 1];
-  __shared__ SnMeta msh_all[SOLVE_WARPS][16];
+  __shared__ int tk_sh[SOLVE_WORKERS];
+  __shared__ SnMeta msh_all[SOLVE_WORKERS][16];
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     A.ctr[(A.epoch + 1) & 1] = 0;
     A.ctr[2 + ((A.epoch + 1) & 1)] = 0;
   }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double* xr = smem + (size_t)warp * (A.max_m + 64 + 16 * 33);
+  const int lane = threadIdx.x % LW, wk = threadIdx.x / LW;
+  double* xr = smem + (size_t)wk * (A.max_m + 64 + RED_SZ);
   double* tv = xr + A.max_m;
   double* red = tv + 64;
-  int* ridx = reinterpret_cast<int*>(smem + (size_t)SOLVE_WARPS * (A.max_m + 64 + 16 * 33) + A.max_m + 128) +
-              warp * A.max_m;
-  // CTA mode: top queue in reverse level order
-  double* cx = smem + (size_t)SOLVE_WARPS * (A.max_m + 64 + 16 * 33);
-  for (; A.ntop > 0;) {
-    const int t = cta_ticket(&A.ctr[2 + (A.epoch & 1)], &tk_sh[SOLVE_WARPS]);
-    if (t >= A.ntop * A.B) break;
-    const int s = A.top[A.ntop - 1 - t / A.B], b = t % A.B;
-    int* done = A.done_all + (int64_t)b * A.ns;
-    if (!(A.skip && A.skip[b])) {
-      bwd_cta_step(S, A, s, b, cx, cx + A.max_m, cx + A.max_m + 64, red, done);
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) st_release(done + s, A.epoch);
-  }
-  __syncthreads();
-  // warp mode: bottom queue, chunks in reverse topological order
+  int* ridx = reinterpret_cast<int*>(smem + (size_t)SOLVE_WORKERS * (A.max_m + 64 + RED_SZ)) + wk * A.max_m;
+  SnMeta* msh = msh_all[wk];
+  // bottom queue, chunks in reverse topological order
   for (;;) {
-    const int t = warp_ticket(&A.ctr[A.epoch & 1], lane, &tk_sh[warp]);
+    const int t = warp_ticket(&A.ctr[A.epoch & 1], lane, &tk_sh[wk]);
     if (t >= A.nchunk * A.B) break;
     const int ch = A.nchunk - 1 - t / A.B, b = t % A.B;
     int* done = A.done_all + (int64_t)b * A.ns;
     const bool sk = A.skip && A.skip[b];
     const int q0 = A.chunk_ptr[ch], n = A.chunk_ptr[ch + 1] - q0;
-    SnMeta* msh = msh_all[warp];
     if (!sk) warp_stage_chunk(S, A, q0, n, b, lane, msh, true);
     for (int j = n - 1; j >= 0; --j) {
       const int s = sk ? A.queue[q0 + j] : msh[j].pad1;
       if (!sk) {
         bwd_warp_step(S, A, msh[j], s, b, lane, xr, tv, red, ridx, done);
-        __syncwarp();
+        wsync();
       }
       if (lane == 0) st_release(done + s, A.epoch);
     }
-    __syncwarp();
+    wsync();
   }
 }
 
