@@ -669,7 +669,7 @@ ckkt_status setup_device(ckkt_ctx* c) {
   }
   c->S = SymDev{nullptr, nullptr, sfirst, srowptr, srows, pofs, level_list, ch_ptr, ch_list, relofs, relmap, uofs, vofs,
                 kp, kmap, perm2, sparent, relw};
-  {  // tiny supernodes (m <= TINY_M, w <= TINY_W, all descendants tiny): one thread per tiny subtree
+  {  // tiny supernodes (m <= TINY_M, w <= TINY_W, all descendants tiny): one lane group per tiny subtree
     const int ns = A.ns;
     c->tiny_host.assign(ns, 0);
     std::vector<int8_t>& T = c->tiny_host;

@@ -1007,7 +1007,7 @@ __global__ void __launch_bounds__(TOP_THREADS, TOP_MINB) k_bwd_top(SymDev S, Swe
 #define CKKT_TINY_M 32
 #endif
 #ifndef CKKT_TINY_W
-#define CKKT_TINY_W 4
+#define CKKT_TINY_W 6
 #endif
 constexpr int TINY_M = CKKT_TINY_M, TINY_W = CKKT_TINY_W;
 
@@ -1141,7 +1141,10 @@ __global__ void __launch_bounds__(256)
 // front panel (m <= 32 rows, w <= 4 columns, ld 32) in the group's shared memory, rows over lanes.
 // Same arithmetic as the big fronts: assemble A + children's panel parts, Cholesky of
 // the w columns, U_s = -L21 L21^T plus the children's trailing parts, L11 <- L11^{-1}.
-constexpr int FT_THREADS = 256;
+#ifndef CKKT_FT_THREADS
+#define CKKT_FT_THREADS 128
+#endif
+constexpr int FT_THREADS = CKKT_FT_THREADS;
 
 __global__ void k_epoch_bump(int* epoch_dev) {  // sweeps without tiny subtrees
   epoch_dev[0] += 1;
