@@ -21,6 +21,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/ckkt.h"
@@ -61,8 +62,11 @@ inline unsigned nblk(int64_t n, int t = TPB) { return (unsigned)((n + t - 1) / t
 // a1: condensation.  One thread per K slot of the internal lower CSC; the sum order is fixed
 // by the maps (W terms, diagonal, J^T D J product terms in row order).
 // ------------------------------------------------------------------------------------------
-__global__ void k_condense(int64_t nnzk, const int64_t* __restrict__ wt_ptr, const int32_t* __restrict__ wt_idx,
-                           const int64_t* __restrict__ jt_ptr, const int32_t* __restrict__ jt_a,
+// IDX: index type of the slot pointers (int32 when every offset fits); MODE: 1 = all product terms
+// are G rows (HyKKT: gamma), 2 = all are H rows (Lifted: D_s[r]), 0 = mixed (jt_r decides)
+template <typename IDX, int MODE>
+__global__ void k_condense(int64_t nnzk, const IDX* __restrict__ wt_ptr, const int32_t* __restrict__ wt_idx,
+                           const IDX* __restrict__ jt_ptr, const int32_t* __restrict__ jt_a,
                            const int32_t* __restrict__ jt_b, const int32_t* __restrict__ jt_r,
                            const int32_t* __restrict__ kdiag, const double* __restrict__ w_val, int64_t w_nnz,
                            const double* __restrict__ g_val, int64_t g_nnz, const double* __restrict__ h_val,
@@ -76,13 +80,17 @@ __global__ void k_condense(int64_t nnzk, const int64_t* __restrict__ wt_ptr, con
   const double* g = g_val + b * g_nnz;
   const double* h = h_val + b * h_nnz;
   double acc = 0.0;
-  for (int64_t t = wt_ptr[k]; t < wt_ptr[k + 1]; ++t) acc += w[wt_idx[t]];
+  for (IDX t = wt_ptr[k]; t < wt_ptr[k + 1]; ++t) acc += w[wt_idx[t]];
   const int dv = kdiag[k];
   if (dv >= 0) acc += sigma[(int64_t)b * n + dv] + (delta ? delta[b] : 0.0);
-  for (int64_t t = jt_ptr[k]; t < jt_ptr[k + 1]; ++t) {
-    const int r = jt_r[t];
-    if (r < me) acc += gamma * (g[jt_a[t]] * g[jt_b[t]]);
-    else acc += d_s[(int64_t)b * mi + (r - me)] * (h[jt_a[t]] * h[jt_b[t]]);
+  for (IDX t = jt_ptr[k]; t < jt_ptr[k + 1]; ++t) {
+    if (MODE == 1) {
+      acc += gamma * (g[jt_a[t]] * g[jt_b[t]]);
+    } else {
+      const int r = jt_r[t];
+      if (MODE == 0 && r < me) acc += gamma * (g[jt_a[t]] * g[jt_b[t]]);
+      else acc += d_s[(int64_t)b * mi + (r - me)] * (h[jt_a[t]] * h[jt_b[t]]);
+    }
   }
   Kval[b * nnzk + k] = acc;
 }
@@ -511,6 +519,7 @@ struct ckkt_ctx {
   // pattern arrays on device
   SymDev S{};
   int64_t *wt_ptr = nullptr, *jt_ptr = nullptr;
+  int32_t *wt_ptr32 = nullptr, *jt_ptr32 = nullptr;  // 32-bit copies when the offsets fit (less map traffic)
   int32_t *wt_idx = nullptr, *jt_a = nullptr, *jt_b = nullptr, *jt_r = nullptr, *kdiag = nullptr;
   int32_t *gt_ptr = nullptr, *gt_e = nullptr, *gt_r = nullptr, *ht_ptr = nullptr, *ht_e = nullptr, *ht_r = nullptr;
   int32_t *g_rowptr = nullptr, *g_col2 = nullptr, *h_rowptr = nullptr, *h_col2 = nullptr;
@@ -879,6 +888,11 @@ ckkt_status setup_device(ckkt_ctx* c) {
   UP(c->wt_ptr, A.wt_ptr);
   UP(c->wt_idx, A.wt_idx);
   UP(c->jt_ptr, A.jt_ptr);
+  if (A.wt_ptr.back() < INT32_MAX && A.jt_ptr.back() < INT32_MAX) {
+    std::vector<int32_t> w32(A.wt_ptr.begin(), A.wt_ptr.end()), j32(A.jt_ptr.begin(), A.jt_ptr.end());
+    UP(c->wt_ptr32, w32);
+    UP(c->jt_ptr32, j32);
+  }
   UP(c->jt_a, A.jt_a);
   UP(c->jt_b, A.jt_b);
   UP(c->jt_r, A.jt_r);
@@ -1176,10 +1190,28 @@ ckkt_status ckkt_refactor(ckkt_ctx* c, const double* w_val, const double* g_val,
   }
   k_init_flags<<<nblk(B), TPB, 0, st>>>(B, c->notpd, c->minpiv);
   prof_begin(c, 0);
-  k_condense<<<dim3(nblk(c->nnzk), B), TPB, 0, st>>>(c->nnzk, c->wt_ptr, c->wt_idx, c->jt_ptr, c->jt_a, c->jt_b,
-                                                     c->jt_r, c->kdiag, w_val, c->w_nnz, g_val, c->g_nnz, h_val,
-                                                     c->h_nnz, sigma_x, d_s, delta_x, gamma, c->n, c->me, c->mi,
-                                                     c->Kval);
+  {
+    const dim3 gk(nblk(c->nnzk), B);
+    const int mode = (c->mi == 0) ? 1 : (c->me == 0 ? 2 : 0);
+#define CKKT_CONDENSE(IDXP, M)                                                                                      \
+  k_condense<std::remove_const_t<std::remove_pointer_t<decltype(IDXP##wt)>>, M><<<gk, TPB, 0, st>>>(               \
+      c->nnzk, IDXP##wt, c->wt_idx, IDXP##jt, c->jt_a, c->jt_b, c->jt_r, c->kdiag, w_val, c->w_nnz, g_val, c->g_nnz, \
+      h_val, c->h_nnz, sigma_x, d_s, delta_x, gamma, c->n, c->me, c->mi, c->Kval)
+    const int32_t* s32wt = c->wt_ptr32;
+    const int32_t* s32jt = c->jt_ptr32;
+    const int64_t* s64wt = c->wt_ptr;
+    const int64_t* s64jt = c->jt_ptr;
+    if (s32wt) {
+      if (mode == 1) CKKT_CONDENSE(s32, 1);
+      else if (mode == 2) CKKT_CONDENSE(s32, 2);
+      else CKKT_CONDENSE(s32, 0);
+    } else {
+      if (mode == 1) CKKT_CONDENSE(s64, 1);
+      else if (mode == 2) CKKT_CONDENSE(s64, 2);
+      else CKKT_CONDENSE(s64, 0);
+    }
+#undef CKKT_CONDENSE
+  }
   DBG_SYNC("k_condense");
   prof_end(c);
   c->launches += 2;
