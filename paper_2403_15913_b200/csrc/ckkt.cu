@@ -319,8 +319,8 @@ __global__ void k_recover(int mi, int n, const int32_t* __restrict__ rowptr, con
 
 // ------------------------------------------------------------------------------------------
 // a8: residual of K_aug and componentwise backward error.  Row blocks x (internal), s, y, z.
-//  rho = -r - K_aug d ; ratio = |rho| / (|K_aug||d| + |r|).  Writes rho (x block internal order)
-//  and the per-row ratio / |rho| for a max reduction.
+//  rho = -r - K_aug d ; ratio = |rho| / (|K_aug||d| + |r|).  Writes rho (x block internal order);
+//  the per-row ratio and |rho| feed block maxima in the same kernel.
 // ------------------------------------------------------------------------------------------
 struct ResArgs {
   int n, me, mi;
@@ -334,17 +334,10 @@ struct ResArgs {
   const double *r1, *r2, *r3, *r4;  // r1 original order
   const double *dx, *ds, *dy, *dz;  // dx internal
   double *rho1, *rho2, *rho3, *rho4;  // rho1 internal
-  double* ratio;                      // [B, rows]
-  double* absres;                     // [B, rows]
   const int* skip;
 };
 
-__global__ void k_kaug_residual(ResArgs a) {
-  const int64_t rows = (int64_t)a.n + 2 * a.mi + a.me;
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int b = blockIdx.y;
-  if (t >= rows) return;
-  if (a.skip && a.skip[b]) { a.ratio[b * rows + t] = 0.0; a.absres[b * rows + t] = 0.0; return; }
+__device__ __forceinline__ void kaug_residual_row(const ResArgs& a, int b, int64_t t, double& ratio_out, double& abs_out) {
   const int n = a.n, me = a.me, mi = a.mi;
   double res, den;
   if (t < n) {
@@ -421,42 +414,46 @@ __global__ void k_kaug_residual(ResArgs a) {
   }
   double ratio = den > 0.0 ? fabs(res) / den : (res == 0.0 ? 0.0 : INFINITY);
   if (res != res) ratio = INFINITY;
-  a.ratio[b * rows + t] = ratio;
-  a.absres[b * rows + t] = fabs(res);
+  ratio_out = ratio;
+  abs_out = fabs(res);
+}
+
+__device__ __forceinline__ double nanmax(double x, double m) { return (x > m || x != x) ? x : m; }
+
+// rho = -r - K_aug d, one row per thread, and, fused, the maxima over rows of the componentwise
+// ratio |rho_i| / (|K_aug||d| + |r|)_i and of |rho_i|: block maxima, then one atomicMax per block on
+// the bit patterns (both quantities are >= 0 or +NaN, whose bit patterns order like the values;
+// a maximum does not depend on the order, so the result stays deterministic)
+__global__ void k_kaug_residual(ResArgs a, unsigned long long* __restrict__ omega_bits,
+                                unsigned long long* __restrict__ resinf_bits) {
+  __shared__ double red[2][TPB / 32];
+  const int64_t rows = (int64_t)a.n + 2 * a.mi + a.me;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  double mr = 0.0, ma = 0.0;
+  if (t < rows && !(a.skip && a.skip[b])) kaug_residual_row(a, b, t, mr, ma);
+  for (int o = 16; o > 0; o >>= 1) {
+    mr = nanmax(__shfl_down_sync(0xffffffffu, mr, o), mr);
+    ma = nanmax(__shfl_down_sync(0xffffffffu, ma, o), ma);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = mr;
+    red[1][threadIdx.x >> 5] = ma;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t0 = 0.0, t1 = 0.0;
+    for (int k = 0; k < TPB / 32; ++k) {
+      t0 = nanmax(red[0][k], t0);
+      t1 = nanmax(red[1][k], t1);
+    }
+    atomicMax(omega_bits + b, (unsigned long long)__double_as_longlong(fabs(t0)));
+    atomicMax(resinf_bits + b, (unsigned long long)__double_as_longlong(fabs(t1)));
+  }
 }
 
 // per-instance max over rows (two-stage; max is order independent => deterministic)
-__global__ void k_max_partial(int64_t len, const double* __restrict__ v, double* __restrict__ part) {
-  __shared__ double red[TPB / 32];
-  const int b = blockIdx.y;
-  double m = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) {
-    double x = v[b * len + i];
-    m = (x > m || x != x) ? x : m;
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    double y = __shfl_down_sync(0xffffffffu, m, o);
-    m = (y > m || y != y) ? y : m;
-  }
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int k = 0; k < TPB / 32; ++k) t = (red[k] > t || red[k] != red[k]) ? red[k] : t;
-    part[(int64_t)b * gridDim.x + blockIdx.x] = t;
-  }
-}
 
-__global__ void k_max_final(int B, int nb, const double* __restrict__ part, double* __restrict__ out) {
-  int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B) return;
-  double t = 0.0;
-  for (int k = 0; k < nb; ++k) {
-    double x = part[(int64_t)b * nb + k];
-    t = (x > t || x != x) ? x : t;
-  }
-  out[b] = t;
-}
 
 // d_new = d + c for accepted instances; dest <- src where acc[b]
 __global__ void k_axpy_sel(int64_t len, const double* __restrict__ d, const double* __restrict__ c,
@@ -572,7 +569,7 @@ struct ckkt_ctx {
   double *cds = nullptr, *cdy = nullptr, *cdz = nullptr;          // correction blocks
   double *rho1 = nullptr, *rho2 = nullptr, *rho3 = nullptr, *rho4 = nullptr;
   double *rho1b = nullptr, *rho2b = nullptr, *rho3b = nullptr, *rho4b = nullptr;
-  double *ratio = nullptr, *absres = nullptr, *part = nullptr, *omega = nullptr, *resinf = nullptr;
+  double *part = nullptr, *omega = nullptr, *resinf = nullptr;
   double *cg_rr = nullptr, *cg_bn = nullptr, *cg_alpha = nullptr, *cg_beta = nullptr;
   int *cg_done = nullptr, *cg_iters = nullptr, *active = nullptr, *accflag = nullptr, *skipflag = nullptr;
   int* h_pinned_int = nullptr;
@@ -966,9 +963,6 @@ ckkt_status setup_device(ckkt_ctx* c) {
   DALLOC(c->rho2b, Bmi);
   DALLOC(c->rho3b, Bme);
   DALLOC(c->rho4b, Bmi);
-  const size_t rows = (size_t)n + 2 * (size_t)mi + me;
-  DALLOC(c->ratio, (size_t)B * rows);
-  DALLOC(c->absres, (size_t)B * rows);
   DALLOC(c->part, (size_t)B * 1024);
   DALLOC(c->omega, 2 * B);
   DALLOC(c->resinf, 2 * B);
@@ -1479,16 +1473,14 @@ void residual(ckkt_ctx* c, const double* r1, const double* r2, const double* r3,
   a.r1 = r1; a.r2 = r2; a.r3 = r3; a.r4 = r4;
   a.dx = dx; a.ds = ds; a.dy = dy; a.dz = dz;
   a.rho1 = rho1; a.rho2 = rho2; a.rho3 = rho3; a.rho4 = rho4;
-  a.ratio = c->ratio; a.absres = c->absres;
   a.skip = c->notpd;
   cudaStream_t st = c->stream;
   prof_begin(c, 4);
-  k_kaug_residual<<<dim3(nblk(rows), B), TPB, 0, st>>>(a);
-  k_max_partial<<<dim3(DOT_BLOCKS, B), TPB, 0, st>>>(rows, c->ratio, c->part);
-  k_max_final<<<nblk(B), TPB, 0, st>>>(B, DOT_BLOCKS, c->part, omega);
-  k_max_partial<<<dim3(DOT_BLOCKS, B), TPB, 0, st>>>(rows, c->absres, c->part);
-  k_max_final<<<nblk(B), TPB, 0, st>>>(B, DOT_BLOCKS, c->part, resinf);
-  c->launches += 5;
+  cudaMemsetAsync(omega, 0, sizeof(double) * B, st);
+  cudaMemsetAsync(resinf, 0, sizeof(double) * B, st);
+  k_kaug_residual<<<dim3(nblk(rows), B), TPB, 0, st>>>(a, reinterpret_cast<unsigned long long*>(omega),
+                                                       reinterpret_cast<unsigned long long*>(resinf));
+  c->launches += 1;
   prof_end(c);
 }
 
