@@ -279,6 +279,112 @@ __global__ void k_cg_init_scalars(int B, const double* __restrict__ part, double
   done[b] = (t == 0.0) || (skip && skip[b]);
 }
 
+// ---- Init-CG for the correction passes: the conjugate directions p_i of the first pass and
+// q_i = S p_i are kept (up to KREC per instance); a correction pass starts from the S-orthogonal
+// projection of its solution onto span{p_i}:  x0 = sum_i c_i p_i,  r0 = b - sum_i c_i q_i,
+// c_i = p_i.b / p_i.q_i  (p_i.q_j = 0 for i != j by conjugacy).  Same operator, same stopping
+// test ||r|| <= rtol ||b|| — only the start changes (R6).
+constexpr int KREC = 32;
+
+// store p, q and p.q of the current iteration into slot iters[b] (first pass only: *enable)
+__global__ void k_cg_store(int me, int B, const double* __restrict__ p, const double* __restrict__ q,
+                           const double* __restrict__ part, const int* __restrict__ iters,
+                           const int* __restrict__ done, const int* __restrict__ enable, double* __restrict__ P,
+                           double* __restrict__ Q, double* __restrict__ PQ) {
+  if (!*enable) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (done[b]) return;
+  const int k = iters[b];
+  if (k >= KREC) return;
+  const int64_t slot = ((int64_t)k * B + b) * me;
+  if (i < me) {
+    P[slot + i] = p[(int64_t)b * me + i];
+    Q[slot + i] = q[(int64_t)b * me + i];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) PQ[(int64_t)k * B + b] = sum_parts(part + (int64_t)b * DOT_BLOCKS, DOT_BLOCKS);
+}
+
+// partial sums of p_i . b for all stored i (rows strided over DOT_BLOCKS blocks)
+__global__ void k_rec_dots(int me, int B, const double* __restrict__ P, const double* __restrict__ bvec,
+                           const int* __restrict__ nrec, const int* __restrict__ skip, double* __restrict__ part) {
+  __shared__ double red[KREC][TPB / 32];
+  const int b = blockIdx.y;
+  const int nk = (skip && skip[b]) ? 0 : nrec[b];
+  double acc[KREC];
+#pragma unroll
+  for (int k = 0; k < KREC; ++k) acc[k] = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < me; i += (int64_t)gridDim.x * blockDim.x) {
+    const double bi = bvec[(int64_t)b * me + i];
+#pragma unroll
+    for (int k = 0; k < KREC; ++k)
+      if (k < nk) acc[k] += P[((int64_t)k * B + b) * me + i] * bi;
+  }
+#pragma unroll
+  for (int k = 0; k < KREC; ++k) {
+    double v = acc[k];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) red[k][threadIdx.x >> 5] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < KREC) {
+    double t = 0.0;
+    for (int w = 0; w < TPB / 32; ++w) t += red[threadIdx.x][w];
+    part[((int64_t)b * KREC + threadIdx.x) * DOT_BLOCKS + blockIdx.x] = t;
+  }
+}
+
+// c_i = (p_i . b) / (p_i . q_i)
+__global__ void k_rec_coef(int B, const double* __restrict__ part, const double* __restrict__ PQ,
+                           const int* __restrict__ nrec, const int* __restrict__ skip, double* __restrict__ coef) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= B * KREC) return;
+  const int b = t / KREC, k = t % KREC;
+  const int nk = (skip && skip[b]) ? 0 : nrec[b];
+  coef[t] = (k < nk) ? sum_parts(part + (int64_t)t * DOT_BLOCKS, DOT_BLOCKS) / PQ[(int64_t)k * B + b] : 0.0;
+}
+
+// x0 = sum c_i p_i, r0 = p0 = b - sum c_i q_i
+__global__ void k_rec_start(int me, int B, const double* __restrict__ P, const double* __restrict__ Q,
+                            const double* __restrict__ coef, const int* __restrict__ nrec,
+                            const double* __restrict__ bvec, double* __restrict__ x, double* __restrict__ r,
+                            double* __restrict__ p) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (i >= me) return;
+  const int nk = nrec[b];
+  const int64_t o = (int64_t)b * me + i;
+  double xs = 0.0, rs = bvec[o];
+  for (int k = 0; k < nk; ++k) {
+    const double ck = coef[b * KREC + k];
+    const int64_t so = ((int64_t)k * B + b) * me + i;
+    xs += ck * P[so];
+    rs -= ck * Q[so];
+  }
+  x[o] = xs;
+  r[o] = rs;
+  p[o] = rs;
+}
+
+__global__ void k_rec_count(int B, const int* __restrict__ iters, int* __restrict__ nrec) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < B) nrec[b] = min(iters[b], KREC);
+}
+
+// CG init from r0: rr = r0.r0 (part), bnorm2 = b.b (part_b); done if converged already
+__global__ void k_cg_init_scalars2(int B, const double* __restrict__ part, const double* __restrict__ part_b,
+                                   double rtol, double* __restrict__ rr, double* __restrict__ bnorm2,
+                                   int* __restrict__ done, int* __restrict__ iters, const int* __restrict__ skip) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const double t = sum_parts(part + (int64_t)b * DOT_BLOCKS, DOT_BLOCKS);
+  const double bb = sum_parts(part_b + (int64_t)b * DOT_BLOCKS, DOT_BLOCKS);
+  rr[b] = t;
+  bnorm2[b] = bb;
+  iters[b] = 0;
+  done[b] = (bb == 0.0) || (skip && skip[b]) || (sqrt(t) <= rtol * sqrt(bb));
+}
+
 // end of a CG iteration inside the graph loop: continue while some instance is active and the cap
 // is not reached; resets the activity counter for the next iteration
 __global__ void k_cg_cond(int* active, int* loop, int maxit, cudaGraphConditionalHandle h) {
@@ -548,6 +654,11 @@ struct ckkt_ctx {
   cudaGraphExec_t cg_exec = nullptr;
   cudaGraphConditionalHandle cg_cond = 0;
   int* cg_loop = nullptr;  // [1] iterations executed by the graph loop
+  // Init-CG: directions of the first pass (KREC slots x B x m_e), p.q, counts, coefficients
+  double *rec_P = nullptr, *rec_Q = nullptr, *rec_PQ = nullptr, *rec_part = nullptr, *rec_coef = nullptr;
+  double* part_b = nullptr;
+  int *rec_enable = nullptr, *rec_n = nullptr;
+  bool rec_on = false;
   int64_t cg_body_launches = 0;
   bool graph_failed = false;
   bool graph_pending_loops = false;  // h_pinned_int[4B] holds the loop count of the last graph launch
@@ -974,6 +1085,17 @@ ckkt_status setup_device(ckkt_ctx* c) {
   DALLOC(c->cg_iters, B);
   DALLOC(c->active, 1);
   DALLOC(c->cg_loop, 1);
+  if (me > 0 && !getenv("CKKT_NO_INITCG")) {  // Init-CG storage (2 KREC m_e doubles per instance)
+    c->rec_on = true;
+    DALLOC(c->rec_P, (size_t)KREC * B * me);
+    DALLOC(c->rec_Q, (size_t)KREC * B * me);
+    DALLOC(c->rec_PQ, (size_t)KREC * B);
+    DALLOC(c->rec_part, (size_t)B * KREC * DOT_BLOCKS);
+    DALLOC(c->rec_coef, (size_t)B * KREC);
+    DALLOC(c->rec_n, B);
+    DALLOC(c->part_b, (size_t)B * 1024);
+  }
+  DALLOC(c->rec_enable, 1);
   DALLOC(c->accflag, B);
   DALLOC(c->skipflag, B);
   CK(cudaMallocHost(&c->h_pinned_int, sizeof(int) * (5 * B + 16)));
@@ -1332,6 +1454,11 @@ void cg_iteration(ckkt_ctx* c) {
                                 c->cg_done);
   dot(c, me, c->cg_p, c->cg_q, c->cg_done);
   k_cg_alpha<<<nblk(B), TPB, 0, st>>>(B, c->part, c->cg_rr, c->cg_alpha, c->cg_done);
+  if (c->rec_on) {
+    k_cg_store<<<gme, TPB, 0, st>>>(me, B, c->cg_p, c->cg_q, c->part, c->cg_iters, c->cg_done, c->rec_enable,
+                                    c->rec_P, c->rec_Q, c->rec_PQ);
+    c->launches++;
+  }
   k_cg_update_xr<<<gme, TPB, 0, st>>>(me, c->cg_alpha, c->cg_p, c->cg_q, c->cg_x, c->cg_r, c->cg_done);
   dot(c, me, c->cg_r, c->cg_r, c->cg_done);
   k_cg_beta<<<nblk(B), TPB, 0, st>>>(B, c->part, c->cg_rr, c->cg_bn, c->opt.cg_rtol, c->cg_beta, c->cg_done,
@@ -1372,7 +1499,7 @@ bool build_cg_graph(ckkt_ctx* c) {
 // writes dx (internal), ds, dy, dz.  Returns the total CG iterations (host copy, per instance) via c->cg_iters.
 ckkt_status solve_pass(ckkt_ctx* c, const double* r1, int r1_internal, const double* r2, const double* r3,
                        const double* r4, double* dx, double* ds, double* dy, double* dz, const int* skip,
-                       std::vector<int>& kcg) {
+                       std::vector<int>& kcg, bool first_pass) {
   const int n = c->n, me = c->me, mi = c->mi, B = c->B;
   cudaStream_t st = c->stream;
   const double gamma = (c->opt.strategy == CKKT_HYKKT) ? c->opt.gamma : 0.0;
@@ -1392,13 +1519,26 @@ ckkt_status solve_pass(ckkt_ctx* c, const double* r1, int r1_internal, const dou
     prof_begin(c, 4);
     k_g_spmv<<<gme, TPB, 0, st>>>(me, n, c->g_rowptr, c->g_col2, c->g_val, c->g_nnz, c->tn, -1.0, r3, 1.0, c->bvec,
                                   skip);
-    // CG: x = 0, r = p = b
-    k_zero<<<gme, TPB, 0, st>>>(me, c->cg_x);
-    cudaMemcpyAsync(c->cg_r, c->bvec, sizeof(double) * (size_t)B * me, cudaMemcpyDeviceToDevice, st);
-    cudaMemcpyAsync(c->cg_p, c->bvec, sizeof(double) * (size_t)B * me, cudaMemcpyDeviceToDevice, st);
-    dot(c, me, c->bvec, c->bvec, skip);
-    k_cg_init_scalars<<<nblk(B), TPB, 0, st>>>(B, c->part, c->cg_rr, c->cg_bn, c->cg_done, c->cg_iters, skip);
-    c->launches += 4;
+    const bool init_cg = c->rec_on && !first_pass;
+    if (c->rec_on) CK(cudaMemsetAsync(c->rec_enable, first_pass ? 1 : 0, sizeof(int), st));
+    if (!init_cg) {  // CG: x = 0, r = p = b
+      k_zero<<<gme, TPB, 0, st>>>(me, c->cg_x);
+      cudaMemcpyAsync(c->cg_r, c->bvec, sizeof(double) * (size_t)B * me, cudaMemcpyDeviceToDevice, st);
+      cudaMemcpyAsync(c->cg_p, c->bvec, sizeof(double) * (size_t)B * me, cudaMemcpyDeviceToDevice, st);
+      dot(c, me, c->bvec, c->bvec, skip);
+      k_cg_init_scalars<<<nblk(B), TPB, 0, st>>>(B, c->part, c->cg_rr, c->cg_bn, c->cg_done, c->cg_iters, skip);
+      c->launches += 4;
+    } else {  // Init-CG: start from the projection onto the first pass's directions
+      k_rec_dots<<<dim3(DOT_BLOCKS, B), TPB, 0, st>>>(me, B, c->rec_P, c->bvec, c->rec_n, skip, c->rec_part);
+      k_rec_coef<<<nblk(B * KREC), TPB, 0, st>>>(B, c->rec_part, c->rec_PQ, c->rec_n, skip, c->rec_coef);
+      k_rec_start<<<gme, TPB, 0, st>>>(me, B, c->rec_P, c->rec_Q, c->rec_coef, c->rec_n, c->bvec, c->cg_x, c->cg_r,
+                                       c->cg_p);
+      k_dot_partial<<<dim3(DOT_BLOCKS, c->B), TPB, 0, st>>>(me, c->bvec, c->bvec, c->part_b, skip);
+      dot(c, me, c->cg_r, c->cg_r, skip);
+      k_cg_init_scalars2<<<nblk(B), TPB, 0, st>>>(B, c->part, c->part_b, c->opt.cg_rtol, c->cg_rr, c->cg_bn,
+                                                  c->cg_done, c->cg_iters, skip);
+      c->launches += 6;
+    }
     prof_end(c);
     const bool use_graph = !c->profiling && !c->graph_failed && !sync_debug() && !getenv("CKKT_NO_GRAPH");
     if (use_graph && !c->cg_exec && !build_cg_graph(c)) {
@@ -1420,6 +1560,10 @@ ckkt_status solve_pass(ckkt_ctx* c, const double* r1, int r1_internal, const dou
         CK(cudaStreamSynchronize(st));
         if (*h_active == 0) break;
       }
+    }
+    if (c->rec_on && first_pass) {
+      k_rec_count<<<nblk(B), TPB, 0, st>>>(B, c->cg_iters, c->rec_n);
+      c->launches++;
     }
     // dy = x ; dx = K^{-1}(-r_gamma - G^T dy)
     prof_begin(c, 4);
@@ -1496,7 +1640,7 @@ extern "C" ckkt_status ckkt_solve(ckkt_ctx* c, const double* r1, const double* r
   const dim3 gn(nblk(n), B), gme(nblk(std::max(me, 1)), B), gmi(nblk(std::max(mi, 1)), B);
   std::vector<int> kcg, kcg_total(B, 0), nref(B, 0);
   // unrefined pass: step in (dxi, ds, dy, dz)
-  ckkt_status s = solve_pass(c, r1, 0, r2, r3, r4, c->dxi, ds, dy, dz, c->notpd, kcg);
+  ckkt_status s = solve_pass(c, r1, 0, r2, r3, r4, c->dxi, ds, dy, dz, c->notpd, kcg, true);
   if (s != CKKT_OK) return s;
   for (int b = 0; b < B; ++b) kcg_total[b] = kcg[b];
   std::vector<int> kcg0 = kcg;
@@ -1530,7 +1674,8 @@ extern "C" ckkt_status ckkt_solve(ckkt_ctx* c, const double* r1, const double* r
     if (me) k_copy_neg<<<gme, TPB, 0, st>>>(me, c->rho3, -1.0, c->rho3b);
     c->launches += 4;
     prof_end(c);
-    s = solve_pass(c, c->rho1b, 1, c->rho2b, c->rho3b, c->rho4b, c->cdx, c->cds, c->cdy, c->cdz, c->skipflag, kcg);
+    s = solve_pass(c, c->rho1b, 1, c->rho2b, c->rho3b, c->rho4b, c->cdx, c->cds, c->cdy, c->cdz, c->skipflag, kcg,
+                   false);
     if (s != CKKT_OK) return s;
     // trial = d + correction
     prof_begin(c, 4);
