@@ -366,6 +366,43 @@ __global__ void k_rec_start(int me, int B, const double* __restrict__ P, const d
   p[o] = rs;
 }
 
+// z += alpha vn  (dx accumulation: K^{-1} G^T dy = sum_k alpha_k K^{-1} G^T p_k, the vn of each
+// iteration), and (first pass) vn into its Init-CG slot
+__global__ void k_cg_update_z(int n, int B, const double* __restrict__ alpha, const double* __restrict__ vn,
+                              double* __restrict__ z, const int* __restrict__ done, const int* __restrict__ iters,
+                              const int* __restrict__ enable, double* __restrict__ VN) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (i >= n || done[b]) return;
+  const int64_t o = (int64_t)b * n + i;
+  const double v = vn[o];
+  z[o] += alpha[b] * v;
+  if (VN && *enable) {
+    const int k = iters[b];
+    if (k < KREC) VN[((int64_t)k * B + b) * n + i] = v;
+  }
+}
+
+// z0 = sum_i c_i vn_i  (Init-CG start of the dx accumulation), or 0
+__global__ void k_rec_start_z(int n, int B, const double* __restrict__ VN, const double* __restrict__ coef,
+                              const int* __restrict__ nrec, double* __restrict__ z) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (i >= n) return;
+  const int nk = (VN && coef) ? nrec[b] : 0;
+  double zs = 0.0;
+  for (int k = 0; k < nk; ++k) zs += coef[b * KREC + k] * VN[((int64_t)k * B + b) * n + i];
+  z[(int64_t)b * n + i] = zs;
+}
+
+// dx = -t - z
+__global__ void k_dx_from_acc(int64_t len, const double* __restrict__ t, const double* __restrict__ z,
+                              double* __restrict__ dx) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (i < len) dx[b * len + i] = -t[b * len + i] - z[b * len + i];
+}
+
 __global__ void k_rec_count(int B, const int* __restrict__ iters, int* __restrict__ nrec) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b < B) nrec[b] = min(iters[b], KREC);
@@ -657,6 +694,7 @@ struct ckkt_ctx {
   // Init-CG: directions of the first pass (KREC slots x B x m_e), p.q, counts, coefficients
   double *rec_P = nullptr, *rec_Q = nullptr, *rec_PQ = nullptr, *rec_part = nullptr, *rec_coef = nullptr;
   double* part_b = nullptr;
+  double *rec_VN = nullptr, *cg_z = nullptr;  // Init-CG vn slots; dx accumulator [B,n]
   int *rec_enable = nullptr, *rec_n = nullptr;
   bool rec_on = false;
   int64_t cg_body_launches = 0;
@@ -1094,7 +1132,9 @@ ckkt_status setup_device(ckkt_ctx* c) {
     DALLOC(c->rec_coef, (size_t)B * KREC);
     DALLOC(c->rec_n, B);
     DALLOC(c->part_b, (size_t)B * 1024);
+    DALLOC(c->rec_VN, (size_t)KREC * B * n);
   }
+  if (me > 0) DALLOC(c->cg_z, (size_t)B * n);
   DALLOC(c->rec_enable, 1);
   DALLOC(c->accflag, B);
   DALLOC(c->skipflag, B);
@@ -1460,6 +1500,9 @@ void cg_iteration(ckkt_ctx* c) {
     c->launches++;
   }
   k_cg_update_xr<<<gme, TPB, 0, st>>>(me, c->cg_alpha, c->cg_p, c->cg_q, c->cg_x, c->cg_r, c->cg_done);
+  k_cg_update_z<<<gn, TPB, 0, st>>>(n, B, c->cg_alpha, c->vn, c->cg_z, c->cg_done, c->cg_iters, c->rec_enable,
+                                    c->rec_VN);
+  c->launches++;
   dot(c, me, c->cg_r, c->cg_r, c->cg_done);
   k_cg_beta<<<nblk(B), TPB, 0, st>>>(B, c->part, c->cg_rr, c->cg_bn, c->opt.cg_rtol, c->cg_beta, c->cg_done,
                                      c->cg_iters, c->active);
@@ -1527,7 +1570,8 @@ ckkt_status solve_pass(ckkt_ctx* c, const double* r1, int r1_internal, const dou
       cudaMemcpyAsync(c->cg_p, c->bvec, sizeof(double) * (size_t)B * me, cudaMemcpyDeviceToDevice, st);
       dot(c, me, c->bvec, c->bvec, skip);
       k_cg_init_scalars<<<nblk(B), TPB, 0, st>>>(B, c->part, c->cg_rr, c->cg_bn, c->cg_done, c->cg_iters, skip);
-      c->launches += 4;
+      k_zero<<<gn, TPB, 0, st>>>(n, c->cg_z);
+      c->launches += 5;
     } else {  // Init-CG: start from the projection onto the first pass's directions
       k_rec_dots<<<dim3(DOT_BLOCKS, B), TPB, 0, st>>>(me, B, c->rec_P, c->bvec, c->rec_n, skip, c->rec_part);
       k_rec_coef<<<nblk(B * KREC), TPB, 0, st>>>(B, c->rec_part, c->rec_PQ, c->rec_n, skip, c->rec_coef);
@@ -1537,7 +1581,8 @@ ckkt_status solve_pass(ckkt_ctx* c, const double* r1, int r1_internal, const dou
       dot(c, me, c->cg_r, c->cg_r, skip);
       k_cg_init_scalars2<<<nblk(B), TPB, 0, st>>>(B, c->part, c->part_b, c->opt.cg_rtol, c->cg_rr, c->cg_bn,
                                                   c->cg_done, c->cg_iters, skip);
-      c->launches += 6;
+      k_rec_start_z<<<gn, TPB, 0, st>>>(n, B, c->rec_VN, c->rec_coef, c->rec_n, c->cg_z);
+      c->launches += 7;
     }
     prof_end(c);
     const bool use_graph = !c->profiling && !c->graph_failed && !sync_debug() && !getenv("CKKT_NO_GRAPH");
@@ -1565,14 +1610,13 @@ ckkt_status solve_pass(ckkt_ctx* c, const double* r1, int r1_internal, const dou
       k_rec_count<<<nblk(B), TPB, 0, st>>>(B, c->cg_iters, c->rec_n);
       c->launches++;
     }
-    // dy = x ; dx = K^{-1}(-r_gamma - G^T dy)
+    // dy = x ; dx = K^{-1}(-r_gamma - G^T dy) = -t - sum_k alpha_k vn_k
     prof_begin(c, 4);
     cudaMemcpyAsync(dy, c->cg_x, sizeof(double) * (size_t)B * me, cudaMemcpyDeviceToDevice, st);
-    k_gt_spmv<<<gn, TPB, 0, st>>>(n, me, c->gt_ptr, c->gt_e, c->gt_r, c->gtv, c->g_nnz, dy, -1.0, c->rg, -1.0, dx,
-                                  skip);
+    // dx = -t - K^{-1} G^T dy with K^{-1} G^T dy accumulated during CG (no extra sweep pair)
+    k_dx_from_acc<<<gn, TPB, 0, st>>>(n, c->tn, c->cg_z, dx);
     c->launches++;
     prof_end(c);
-    ksolve(c, dx, skip);
     int* h_iters = c->h_pinned_int + 3 * B;
     CK(cudaMemcpyAsync(h_iters, c->cg_iters, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));

@@ -13,8 +13,8 @@ class RecCG(OK.SparseKKT):
         x = np.zeros(self.m_e)
         if bnorm == 0.0:
             return x, 0, True
-        store = not hasattr(self, 'P')
-        if not store and self.mode != 'plain':
+        store = not hasattr(self, 'P') or self.mode == 'init2'
+        if hasattr(self, 'P') and self.mode != 'plain':
             # x0 = P (P^T S P)^{-1} P^T b with S p_i = q_i, P^T S P diagonal (CG conjugacy)
             for p, q, pq in zip(self.P, self.Q, self.PQ):
                 x += (p @ b) / pq * p
@@ -22,7 +22,7 @@ class RecCG(OK.SparseKKT):
         else:
             r = b.copy()
         if store:
-            self.P, self.Q, self.PQ = [], [], []
+            self.P, self.Q, self.PQ = [], [], []  # (init2: each pass replaces the store)
         p = r.copy(); rr = r @ r
         for k in range(1, self.cg_maxit + 1):
             if np.sqrt(rr) <= self.cg_rtol * bnorm:
@@ -31,9 +31,8 @@ class RecCG(OK.SparseKKT):
             pq = p @ q
             if store:
                 self.P.append(p.copy()); self.Q.append(q.copy()); self.PQ.append(pq)
-            elif self.mode == 'deflated':
-                # keep the new direction S-orthogonal to the stored ones (augmented CG)
-                pass
+            if not store and self.mode == 'aug' and getattr(self, 'append', False) and len(self.P) < 64:
+                self.P2.append(p.copy()); self.Q2.append(q.copy()); self.PQ2.append(pq)
             alpha = rr / pq
             x += alpha * p
             r -= alpha * q
@@ -41,12 +40,16 @@ class RecCG(OK.SparseKKT):
             if np.sqrt(rr_new) <= self.cg_rtol * bnorm:
                 return x, k, True
             p = r + (rr_new / rr) * p
+            if not store and self.mode == 'aug':
+                # AugCG: keep the new direction S-conjugate to the stored ones
+                for pi, qi, pqi in zip(self.P, self.Q, self.PQ):
+                    p -= (qi @ r) / pqi * pi
             rr = rr_new
         return x, self.cg_maxit, False
 
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 200
 case = distillation_case(N, 1, iterates=[3, 9, 15])
-for mode in ['plain', 'init']:
+for mode in (sys.argv[2].split(',') if len(sys.argv) > 2 else ['plain', 'init', 'aug']):
     for b in range(case.B):
         o = RecCG(case.n, case.m_e, case.m_i, case.w_row, case.w_col, case.g_rowptr, case.g_col, E32, E32[:0],
                   strategy=1, gamma=1e7, leaf=1072)
