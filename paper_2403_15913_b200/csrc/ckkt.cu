@@ -204,29 +204,37 @@ __global__ void k_dot_partial(int64_t len, const double* __restrict__ a, const d
 
 constexpr int DOT_BLOCKS = 592;  // 4 per SM: enough loads in flight for the n-long dot products
 
-// fixed-order sum of a block-partials row (four interleaved partial sums)
-__device__ __forceinline__ double sum_parts(const double* __restrict__ p, int nb) {
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-  int k = 0;
-  for (; k + 3 < nb; k += 4) {
-    s0 += p[k];
-    s1 += p[k + 1];
-    s2 += p[k + 2];
-    s3 += p[k + 3];
+
+// Fixed-order sum of a block-partials row by a whole block (TPB threads, one block per row):
+// thread t adds rows t, t + TPB, ..., then a shared-memory tree.  Every thread gets the sum.
+__device__ __forceinline__ double block_sum_parts(const double* __restrict__ p, int nb) {
+  __shared__ double sh[TPB];
+  __syncthreads();  // (sh may be reused by a previous call)
+  double v = 0.0;
+  for (int k = threadIdx.x; k < nb; k += TPB) v += p[k];
+  sh[threadIdx.x] = v;
+  __syncthreads();
+  for (int o = TPB / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
   }
-  for (; k < nb; ++k) s0 += p[k];
-  return (s0 + s1) + (s2 + s3);
+  return sh[0];
 }
 
 // CG scalar step after q = S p:  alpha = rr / (p.q)
 __global__ void k_cg_alpha(int B, const double* __restrict__ part, const double* __restrict__ rr,
-                           double* __restrict__ alpha, const int* __restrict__ done) {
-  int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B) return;
-  if (done[b]) { alpha[b] = 0.0; return; }
-  double pq = 0.0;
-  pq = sum_parts(part + (int64_t)b * DOT_BLOCKS, DOT_BLOCKS);
-  alpha[b] = rr[b] / pq;
+                           double* __restrict__ alpha, const int* __restrict__ done, const int* __restrict__ iters,
+                           const int* __restrict__ rec_enable, double* __restrict__ PQ, int krec) {
+  const int b = blockIdx.x;  // one block per instance
+  if (done[b]) {
+    if (threadIdx.x == 0) alpha[b] = 0.0;
+    return;
+  }
+  const double pq = block_sum_parts(part + (int64_t)b * DOT_BLOCKS, DOT_BLOCKS);
+  if (threadIdx.x == 0) {
+    alpha[b] = rr[b] / pq;
+    if (PQ && *rec_enable && iters[b] < krec) PQ[(int64_t)iters[b] * B + b] = pq;
+  }
 }
 
 __global__ void k_cg_update_xr(int me, const double* __restrict__ alpha, const double* __restrict__ p,
@@ -244,16 +252,19 @@ __global__ void k_cg_update_xr(int me, const double* __restrict__ alpha, const d
 __global__ void k_cg_beta(int B, const double* __restrict__ part, double* __restrict__ rr, const double* __restrict__ bnorm2,
                           double rtol, double* __restrict__ beta, int* __restrict__ done, int* __restrict__ iters,
                           int* __restrict__ active) {
-  int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B) return;
-  if (done[b]) { beta[b] = 0.0; return; }
-  double t = 0.0;
-  t = sum_parts(part + (int64_t)b * DOT_BLOCKS, DOT_BLOCKS);
-  iters[b] += 1;
-  beta[b] = t / rr[b];
-  rr[b] = t;
-  if (sqrt(t) <= rtol * sqrt(bnorm2[b])) done[b] = 1;
-  else atomicAdd(active, 1);
+  const int b = blockIdx.x;  // one block per instance
+  if (done[b]) {
+    if (threadIdx.x == 0) beta[b] = 0.0;
+    return;
+  }
+  const double t = block_sum_parts(part + (int64_t)b * DOT_BLOCKS, DOT_BLOCKS);
+  if (threadIdx.x == 0) {
+    iters[b] += 1;
+    beta[b] = t / rr[b];
+    rr[b] = t;
+    if (sqrt(t) <= rtol * sqrt(bnorm2[b])) done[b] = 1;
+    else atomicAdd(active, 1);
+  }
 }
 
 __global__ void k_cg_update_p(int me, const double* __restrict__ beta, const double* __restrict__ r,
@@ -269,14 +280,14 @@ __global__ void k_cg_update_p(int me, const double* __restrict__ beta, const dou
 __global__ void k_cg_init_scalars(int B, const double* __restrict__ part, double* __restrict__ rr,
                                   double* __restrict__ bnorm2, int* __restrict__ done, int* __restrict__ iters,
                                   const int* __restrict__ skip) {
-  int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B) return;
-  double t = 0.0;
-  t = sum_parts(part + (int64_t)b * DOT_BLOCKS, DOT_BLOCKS);
-  rr[b] = t;
-  bnorm2[b] = t;
-  iters[b] = 0;
-  done[b] = (t == 0.0) || (skip && skip[b]);
+  const int b = blockIdx.x;  // one block per instance
+  const double t = block_sum_parts(part + (int64_t)b * DOT_BLOCKS, DOT_BLOCKS);
+  if (threadIdx.x == 0) {
+    rr[b] = t;
+    bnorm2[b] = t;
+    iters[b] = 0;
+    done[b] = (t == 0.0) || (skip && skip[b]);
+  }
 }
 
 // ---- Init-CG for the correction passes: the conjugate directions p_i of the first pass and
@@ -302,7 +313,6 @@ __global__ void k_cg_store(int me, int B, const double* __restrict__ p, const do
     P[slot + i] = p[(int64_t)b * me + i];
     Q[slot + i] = q[(int64_t)b * me + i];
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) PQ[(int64_t)k * B + b] = sum_parts(part + (int64_t)b * DOT_BLOCKS, DOT_BLOCKS);
 }
 
 // partial sums of p_i . b for all stored i (rows strided over DOT_BLOCKS blocks)
@@ -337,11 +347,15 @@ __global__ void k_rec_dots(int me, int B, const double* __restrict__ P, const do
 // c_i = (p_i . b) / (p_i . q_i)
 __global__ void k_rec_coef(int B, const double* __restrict__ part, const double* __restrict__ PQ,
                            const int* __restrict__ nrec, const int* __restrict__ skip, double* __restrict__ coef) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= B * KREC) return;
+  const int t = blockIdx.x;  // one block per (instance, direction)
   const int b = t / KREC, k = t % KREC;
   const int nk = (skip && skip[b]) ? 0 : nrec[b];
-  coef[t] = (k < nk) ? sum_parts(part + (int64_t)t * DOT_BLOCKS, DOT_BLOCKS) / PQ[(int64_t)k * B + b] : 0.0;
+  if (k >= nk) {
+    if (threadIdx.x == 0) coef[t] = 0.0;
+    return;
+  }
+  const double v = block_sum_parts(part + (int64_t)t * DOT_BLOCKS, DOT_BLOCKS);
+  if (threadIdx.x == 0) coef[t] = v / PQ[(int64_t)k * B + b];
 }
 
 // x0 = sum c_i p_i, r0 = p0 = b - sum c_i q_i
@@ -412,14 +426,15 @@ __global__ void k_rec_count(int B, const int* __restrict__ iters, int* __restric
 __global__ void k_cg_init_scalars2(int B, const double* __restrict__ part, const double* __restrict__ part_b,
                                    double rtol, double* __restrict__ rr, double* __restrict__ bnorm2,
                                    int* __restrict__ done, int* __restrict__ iters, const int* __restrict__ skip) {
-  int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B) return;
-  const double t = sum_parts(part + (int64_t)b * DOT_BLOCKS, DOT_BLOCKS);
-  const double bb = sum_parts(part_b + (int64_t)b * DOT_BLOCKS, DOT_BLOCKS);
-  rr[b] = t;
-  bnorm2[b] = bb;
-  iters[b] = 0;
-  done[b] = (bb == 0.0) || (skip && skip[b]) || (sqrt(t) <= rtol * sqrt(bb));
+  const int b = blockIdx.x;  // one block per instance
+  const double t = block_sum_parts(part + (int64_t)b * DOT_BLOCKS, DOT_BLOCKS);
+  const double bb = block_sum_parts(part_b + (int64_t)b * DOT_BLOCKS, DOT_BLOCKS);
+  if (threadIdx.x == 0) {
+    rr[b] = t;
+    bnorm2[b] = bb;
+    iters[b] = 0;
+    done[b] = (bb == 0.0) || (skip && skip[b]) || (sqrt(t) <= rtol * sqrt(bb));
+  }
 }
 
 // end of a CG iteration inside the graph loop: continue while some instance is active and the cap
@@ -1493,7 +1508,8 @@ void cg_iteration(ckkt_ctx* c) {
   k_g_spmv<<<gme, TPB, 0, st>>>(me, n, c->g_rowptr, c->g_col2, c->g_val, c->g_nnz, c->vn, 1.0, nullptr, 0.0, c->cg_q,
                                 c->cg_done);
   dot(c, me, c->cg_p, c->cg_q, c->cg_done);
-  k_cg_alpha<<<nblk(B), TPB, 0, st>>>(B, c->part, c->cg_rr, c->cg_alpha, c->cg_done);
+  k_cg_alpha<<<B, TPB, 0, st>>>(B, c->part, c->cg_rr, c->cg_alpha, c->cg_done, c->cg_iters, c->rec_enable,
+                                c->rec_PQ, KREC);
   if (c->rec_on) {
     k_cg_store<<<gme, TPB, 0, st>>>(me, B, c->cg_p, c->cg_q, c->part, c->cg_iters, c->cg_done, c->rec_enable,
                                     c->rec_P, c->rec_Q, c->rec_PQ);
@@ -1504,7 +1520,7 @@ void cg_iteration(ckkt_ctx* c) {
                                     c->rec_VN);
   c->launches++;
   dot(c, me, c->cg_r, c->cg_r, c->cg_done);
-  k_cg_beta<<<nblk(B), TPB, 0, st>>>(B, c->part, c->cg_rr, c->cg_bn, c->opt.cg_rtol, c->cg_beta, c->cg_done,
+  k_cg_beta<<<B, TPB, 0, st>>>(B, c->part, c->cg_rr, c->cg_bn, c->opt.cg_rtol, c->cg_beta, c->cg_done,
                                      c->cg_iters, c->active);
   k_cg_update_p<<<gme, TPB, 0, st>>>(me, c->cg_beta, c->cg_r, c->cg_p, c->cg_done);
   c->launches += 7;
@@ -1569,17 +1585,17 @@ ckkt_status solve_pass(ckkt_ctx* c, const double* r1, int r1_internal, const dou
       cudaMemcpyAsync(c->cg_r, c->bvec, sizeof(double) * (size_t)B * me, cudaMemcpyDeviceToDevice, st);
       cudaMemcpyAsync(c->cg_p, c->bvec, sizeof(double) * (size_t)B * me, cudaMemcpyDeviceToDevice, st);
       dot(c, me, c->bvec, c->bvec, skip);
-      k_cg_init_scalars<<<nblk(B), TPB, 0, st>>>(B, c->part, c->cg_rr, c->cg_bn, c->cg_done, c->cg_iters, skip);
+      k_cg_init_scalars<<<B, TPB, 0, st>>>(B, c->part, c->cg_rr, c->cg_bn, c->cg_done, c->cg_iters, skip);
       k_zero<<<gn, TPB, 0, st>>>(n, c->cg_z);
       c->launches += 5;
     } else {  // Init-CG: start from the projection onto the first pass's directions
       k_rec_dots<<<dim3(DOT_BLOCKS, B), TPB, 0, st>>>(me, B, c->rec_P, c->bvec, c->rec_n, skip, c->rec_part);
-      k_rec_coef<<<nblk(B * KREC), TPB, 0, st>>>(B, c->rec_part, c->rec_PQ, c->rec_n, skip, c->rec_coef);
+      k_rec_coef<<<B * KREC, TPB, 0, st>>>(B, c->rec_part, c->rec_PQ, c->rec_n, skip, c->rec_coef);
       k_rec_start<<<gme, TPB, 0, st>>>(me, B, c->rec_P, c->rec_Q, c->rec_coef, c->rec_n, c->bvec, c->cg_x, c->cg_r,
                                        c->cg_p);
       k_dot_partial<<<dim3(DOT_BLOCKS, c->B), TPB, 0, st>>>(me, c->bvec, c->bvec, c->part_b, skip);
       dot(c, me, c->cg_r, c->cg_r, skip);
-      k_cg_init_scalars2<<<nblk(B), TPB, 0, st>>>(B, c->part, c->part_b, c->opt.cg_rtol, c->cg_rr, c->cg_bn,
+      k_cg_init_scalars2<<<B, TPB, 0, st>>>(B, c->part, c->part_b, c->opt.cg_rtol, c->cg_rr, c->cg_bn,
                                                   c->cg_done, c->cg_iters, skip);
       k_rec_start_z<<<gn, TPB, 0, st>>>(n, B, c->rec_VN, c->rec_coef, c->rec_n, c->cg_z);
       c->launches += 7;
