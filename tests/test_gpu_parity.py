@@ -89,6 +89,20 @@ def test_not_pd_flag_matches_oracle():
         assert max(block_errors(g, b, d)) <= STEP_TOL
 
 
+def test_not_pd_instance_in_hykkt_batch():
+    """A non-PD instance in a HyKKT batch: flagged and NaN-filled, while the other instances run the
+    CG (first pass, Init-CG correction passes, accumulated dx) unaffected and match the oracle."""
+    case = random_case(30, 8, 0, seeds=[7, 8, 9])
+    case.sigma_x[1] -= 1e9
+    g = run_gpu(case, 1, gamma=1e4, leaf=8)
+    assert g["notpd"].tolist() == [0, 1, 0]
+    assert np.all(np.isnan(g["dx"][1]))
+    for b in (0, 2):
+        o, d, info = run_oracle(case, b, 1, gamma=1e4, leaf=8)
+        assert max(block_errors(g, b, d)) <= STEP_TOL
+        assert g["info"][b]["rel_res"] <= RES_TOL
+
+
 def test_gamma_sweep_stress():
     """Config 5: Sigma log-uniform over [1e-8, 1e8] on all variables, gamma in 1e4..1e8."""
     case = distillation_case(40, 1, iterates=[12])
