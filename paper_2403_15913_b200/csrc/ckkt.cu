@@ -315,32 +315,25 @@ __global__ void k_cg_store(int me, int B, const double* __restrict__ p, const do
   }
 }
 
-// partial sums of p_i . b for all stored i (rows strided over DOT_BLOCKS blocks)
+// partial sums of p_k . b: block (x, b, k) covers a strided share of the rows of direction k
 __global__ void k_rec_dots(int me, int B, const double* __restrict__ P, const double* __restrict__ bvec,
                            const int* __restrict__ nrec, const int* __restrict__ skip, double* __restrict__ part) {
-  __shared__ double red[KREC][TPB / 32];
-  const int b = blockIdx.y;
+  __shared__ double red[TPB / 32];
+  const int b = blockIdx.y, k = blockIdx.z;
   const int nk = (skip && skip[b]) ? 0 : nrec[b];
-  double acc[KREC];
-#pragma unroll
-  for (int k = 0; k < KREC; ++k) acc[k] = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < me; i += (int64_t)gridDim.x * blockDim.x) {
-    const double bi = bvec[(int64_t)b * me + i];
-#pragma unroll
-    for (int k = 0; k < KREC; ++k)
-      if (k < nk) acc[k] += P[((int64_t)k * B + b) * me + i] * bi;
-  }
-#pragma unroll
-  for (int k = 0; k < KREC; ++k) {
-    double v = acc[k];
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-    if ((threadIdx.x & 31) == 0) red[k][threadIdx.x >> 5] = v;
-  }
+  if (k >= nk) return;  // uniform per block
+  const double* pk = P + ((int64_t)k * B + b) * me;
+  const double* bb = bvec + (int64_t)b * me;
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < me; i += (int64_t)gridDim.x * blockDim.x)
+    acc += pk[i] * bb[i];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
   __syncthreads();
-  if (threadIdx.x < KREC) {
+  if (threadIdx.x == 0) {
     double t = 0.0;
-    for (int w = 0; w < TPB / 32; ++w) t += red[threadIdx.x][w];
-    part[((int64_t)b * KREC + threadIdx.x) * DOT_BLOCKS + blockIdx.x] = t;
+    for (int w = 0; w < TPB / 32; ++w) t += red[w];
+    part[((int64_t)b * KREC + k) * DOT_BLOCKS + blockIdx.x] = t;
   }
 }
 
@@ -1589,7 +1582,7 @@ ckkt_status solve_pass(ckkt_ctx* c, const double* r1, int r1_internal, const dou
       k_zero<<<gn, TPB, 0, st>>>(n, c->cg_z);
       c->launches += 5;
     } else {  // Init-CG: start from the projection onto the first pass's directions
-      k_rec_dots<<<dim3(DOT_BLOCKS, B), TPB, 0, st>>>(me, B, c->rec_P, c->bvec, c->rec_n, skip, c->rec_part);
+      k_rec_dots<<<dim3(DOT_BLOCKS, B, KREC), TPB, 0, st>>>(me, B, c->rec_P, c->bvec, c->rec_n, skip, c->rec_part);
       k_rec_coef<<<B * KREC, TPB, 0, st>>>(B, c->rec_part, c->rec_PQ, c->rec_n, skip, c->rec_coef);
       k_rec_start<<<gme, TPB, 0, st>>>(me, B, c->rec_P, c->rec_Q, c->rec_coef, c->rec_n, c->bvec, c->cg_x, c->cg_r,
                                        c->cg_p);

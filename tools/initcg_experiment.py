@@ -24,6 +24,9 @@ class RecCG(OK.SparseKKT):
         if store:
             self.P, self.Q, self.PQ = [], [], []  # (init2: each pass replaces the store)
         p = r.copy(); rr = r @ r
+        if not store and self.mode == 'aug':
+            for pi, qi, pqi in zip(self.P, self.Q, self.PQ):
+                p -= (qi @ r) / pqi * pi
         for k in range(1, self.cg_maxit + 1):
             if np.sqrt(rr) <= self.cg_rtol * bnorm:
                 return x, k - 1, True
