@@ -677,6 +677,7 @@ struct ckkt_ctx {
   int64_t Usize = 0, Vsize = 0;
   int max_m = 1;
   int ntask = 0, grid_fac = 1, grid_fwd = 1, grid_bwd = 1, grid_ftop = 1, grid_btop = 1;
+  int small_panel = SMALL_PANEL_MIN;  // one-warp front threshold (doubles), chosen at setup
   int epoch_fac = 0, epoch_fwd = 0, epoch_bwd = 0;
   int* epoch_dev = nullptr;  // [2] forward / backward sweep epochs, bumped on the device
   Sched Qfac{}, Qfwd{}, Qbwd{};
@@ -847,13 +848,17 @@ ckkt_status setup_device(ckkt_ctx* c) {
      // small ones (one warp each)
     std::vector<int32_t> tsn, tbig;
     c->big_smem = 0;
+    // many supernodes: more one-warp fronts keep 8 independent fronts in flight per CTA (C3: -2 ms per
+    // refactor); few supernodes: the CTA path finishes the short critical path sooner (C2)
+    c->small_panel = ((int64_t)A.ns * B > 200000) ? SMALL_PANEL_MAX : SMALL_PANEL_MIN;
+    if (const char* e = getenv("CKKT_SMALL_PANEL")) c->small_panel = std::max(64, std::min(SMALL_PANEL_MAX, atoi(e)));
     for (int l = 0; l < A.nlevels; ++l) {
       std::vector<int32_t> small;
       for (int k = A.level_ptr[l]; k < A.level_ptr[l + 1]; ++k) {
         const int s = A.level_list[k];
         if (c->tiny_host[s]) continue;
         const int64_t m = A.srowptr[s + 1] - A.srowptr[s], w = A.sfirst[s + 1] - A.sfirst[s];
-        if (m * w <= SMALL_PANEL && w <= 32) {
+        if (m * w <= c->small_panel && w <= 32) {
           small.push_back(s);
         } else {
           tbig.push_back(1);
@@ -880,10 +885,10 @@ ckkt_status setup_device(ckkt_ctx* c) {
     UP(cfac, z2);
     UP(cfwd, z2);
     UP(cbwd, z2);
-    c->Qfac = Sched{c->ntask, d_tsn, d_tbig, dfac, cfac};
-    c->Qfwd = Sched{c->ntask, d_tsn, d_tbig, dfwd, cfwd};
-    c->Qbwd = Sched{c->ntask, d_tsn, d_tbig, dbwd, cbwd};
-    c->fac_smem = std::max<int64_t>(c->big_smem, 8 * SMALL_WARPS * SMALL_PANEL);
+    c->Qfac = Sched{c->ntask, d_tsn, d_tbig, dfac, cfac, c->small_panel};
+    c->Qfwd = Sched{c->ntask, d_tsn, d_tbig, dfwd, cfwd, c->small_panel};
+    c->Qbwd = Sched{c->ntask, d_tsn, d_tbig, dbwd, cbwd, c->small_panel};
+    c->fac_smem = std::max<int64_t>(c->big_smem, 8 * SMALL_WARPS * c->small_panel);
     c->sol_smem = 8 * ((int64_t)SOLVE_WORKERS * (c->max_m + 64 + RED_SZ)) +
                   4 * (int64_t)SOLVE_WORKERS * c->max_m;  // + per-worker row indices (backward)
     c->fwd_smem = 8 * ((int64_t)SOLVE_WORKERS * (c->max_m + 64));

@@ -173,9 +173,11 @@ __device__ __forceinline__ void dense_blocked(double* Ps, int ldp, int w, int m,
   for (int bi = 1; bi < nb; ++bi) {
     const int oi = NBW * bi, bwi = min(NBW, w - oi);
     const int ntile = bi * 4;  // (j, 2 x 2 tiles of 8 x 8)
-    double keep[2][2];
+    // tiles of block row bi per warp: <= 2 for a CTA of 8 warps, <= 12 for one warp alone (nb <= 4)
+    constexpr int MAXQ = CTA ? 2 : 12;
+    double keep[MAXQ][2];
     // T_ij = sum_k L_ik Z_kj  (B = Z not transposed: b = Z[k][n])
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < MAXQ; ++q) {
       const int tI = warp + q * nwarp;
       keep[q][0] = keep[q][1] = 0.0;
       if (tI < ntile) {
@@ -196,7 +198,7 @@ __device__ __forceinline__ void dense_blocked(double* Ps, int ldp, int w, int m,
       }
     }
     group_sync<CTA>();  // every T of block row bi computed before any L_ij is replaced
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < MAXQ; ++q) {
       const int tI = warp + q * nwarp;
       if (tI < ntile) {
         const int j = tI >> 2, ti = (tI >> 1) & 1, tj = tI & 1;
@@ -209,7 +211,7 @@ __device__ __forceinline__ void dense_blocked(double* Ps, int ldp, int w, int m,
     }
     group_sync<CTA>();
     // Z_ij = -Zd_i T_ij  (A = Zd_i lower with zero upper part, B = T not transposed)
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < MAXQ; ++q) {
       const int tI = warp + q * nwarp;
       keep[q][0] = keep[q][1] = 0.0;
       if (tI < ntile) {
@@ -225,7 +227,7 @@ __device__ __forceinline__ void dense_blocked(double* Ps, int ldp, int w, int m,
       }
     }
     group_sync<CTA>();
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < MAXQ; ++q) {
       const int tI = warp + q * nwarp;
       if (tI < ntile) {
         const int j = tI >> 2, ti = (tI >> 1) & 1, tj = tI & 1;

@@ -21,7 +21,9 @@
 
 #include "dense_front.cuh"
 
-constexpr int SMALL_PANEL = 512;   // doubles of a small supernode panel (m * w)
+// doubles of a small (one-warp) front's panel: chosen per analysis at setup (Sched::small_panel);
+// large trees profit from more one-warp fronts (8 in flight per CTA), small ones from CTA fronts
+constexpr int SMALL_PANEL_MIN = 512, SMALL_PANEL_MAX = 1536;
 constexpr int SMALL_WARPS = 8;     // warps per CTA; small supernodes per task
 constexpr int MF_THREADS = 32 * SMALL_WARPS;
 
@@ -64,6 +66,7 @@ struct Sched {
   const int32_t* task_big;        // [ntask]
   int* done;                      // [B * ns] epoch flags
   int* ctr;                       // [2] ticket counters (alternating per epoch)
+  int small_panel;                // doubles per warp of a small front's shared-memory panel
 };
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
@@ -343,7 +346,7 @@ __global__ void __launch_bounds__(MF_THREADS)
             if (!tiny[S.ch_list[ci]]) wait_epoch(done + S.ch_list[ci], epoch);
         __syncwarp();
         const unsigned long long t1 = gtimer();
-        factor_small(S, s, b, lane, smem + warp * SMALL_PANEL, dsh_all[warp], L, Lsize, Ub, Usize, Kb, notpd, minpiv);
+        factor_small(S, s, b, lane, smem + warp * Q.small_panel, dsh_all[warp], L, Lsize, Ub, Usize, Kb, notpd, minpiv);
         fence_acq_rel();
         __syncwarp();
         if (g_debug_ts && lane == 0 && b == 0) {
