@@ -103,6 +103,16 @@ def test_not_pd_instance_in_hykkt_batch():
         assert g["info"][b]["rel_res"] <= RES_TOL
 
 
+@pytest.mark.parametrize("n,small_panel", [(22, "512"), (30, "1536")])
+def test_one_warp_dense_fronts_wider_than_16(n, small_panel, monkeypatch):
+    """Dense instances whose single front (16 < w <= 32) runs on the one-warp blocked dense path
+    (two 16-column diagonal blocks, Z assembled by one warp)."""
+    monkeypatch.setenv("CKKT_SMALL_PANEL", small_panel)
+    case = random_case(n, 4, 0, seeds=[21, 22], density=1.0)
+    _check(case, 1, gamma=1e4, leaf=n)
+    _check(case, 0, leaf=n) if case.m_i else None
+
+
 def test_gamma_sweep_stress():
     """Config 5: Sigma log-uniform over [1e-8, 1e8] on all variables, gamma in 1e4..1e8."""
     case = distillation_case(40, 1, iterates=[12])

@@ -1,10 +1,10 @@
 #!/bin/bash
 # usage: tools/build_ref_variant.sh <name> <git-ref> ["<-D flags>"]  -> build_variants/<name>/libckkt.so
-set -e
+set -e -o pipefail
 cd /root/repo
 d=build_variants/src_$1
 rm -rf $d; mkdir -p $d/x/csrc $d/include build_variants/$1
-for f in ckkt.cu mf_kernels.cuh analysis.h analysis.cpp; do git show $2:paper_2403_15913_b200/csrc/$f > $d/x/csrc/$f; done
+for f in ckkt.cu mf_kernels.cuh dense_front.cuh analysis.h analysis.cpp; do git show $2:paper_2403_15913_b200/csrc/$f > $d/x/csrc/$f; done
 git show $2:include/ckkt.h > $d/include/ckkt.h
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 -Xptxas -O3 \
   --expt-relaxed-constexpr $3 -c $d/x/csrc/ckkt.cu -o build_variants/$1/ckkt.o 2>&1 | grep -E "error" || true

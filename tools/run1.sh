@@ -1,2 +1,1 @@
-python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -x -q -k "not c3" > gpurun_out/pytest_gpu.log 2>&1; tail -1 gpurun_out/pytest_gpu.log
-python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/b3.json 2> gpurun_out/b3.err; python -c "import json; d=json.load(open('gpurun_out/b3.json')); print(d['value'], d['phases_ms'], d['solver'], d['lifted']['ms_per_iter'])"
+CKKT_LIB_OVERRIDE=build_variants/buggy/libckkt.so python -m pytest tests/test_gpu_parity.py -x -q -k "wider" 2>&1 | tail -3
