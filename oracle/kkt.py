@@ -228,6 +228,33 @@ class SparseKKT:
         return tuple(best[2]), info
 
 
+def inertia_correction(kkt: SparseKKT, w_val, g_val, h_val, sigma_x, d_s, delta_last=0.0,
+                       delta_first=1e-4, kappa_plus=8.0, delta_min=1e-20, delta_max=1e40):
+    """Inertia correction around the refactorization ("(delta_x, delta_c) are computed so
+    as the regularized system satisfies (8)"; Cholesky success <=> correct inertia).
+    Schedule = DESIGN.md reading R13 (SPEC inertia_correction): try delta = 0; on failure start at
+    delta_first * max(1, ||W||_inf) if delta_last == 0, else max(delta_min, delta_last / 3) (kappa_minus = 1/3);
+    multiply by kappa_plus after each further failure; give up above delta_max.
+    Returns (delta, trials, failed)."""
+    delta, trials = 0.0, 0
+    while True:
+        trials += 1
+        if kkt.refactor(w_val, g_val, h_val, sigma_x, d_s, delta) < 0:
+            return delta, trials, False
+        if delta == 0.0:
+            if delta_last == 0.0:
+                w_inf = float(abs(kkt.Wsym).sum(axis=1).max()) if kkt.Wsym.nnz else 0.0   # ||W||_inf
+                # max(1, ||W||_inf); a NaN norm propagates (NaN values never factor: give up)
+                d = delta_first * (w_inf if not w_inf <= 1.0 else 1.0)
+            else:
+                d = max(delta_min, delta_last / 3.0)
+        else:
+            d = kappa_plus * delta
+        if not d <= delta_max:
+            return delta, trials, True
+        delta = d
+
+
 def _gather_csr(K, rows, cols):
     """K[rows[i], cols[i]] for a csr matrix with sorted indices (0 where absent)."""
     out = np.zeros(len(rows))
