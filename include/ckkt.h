@@ -139,6 +139,26 @@ ckkt_status ckkt_refactor(ckkt_ctx *ctx, const double *w_val, const double *g_va
                           const double *sigma_x, const double *d_s, const double *delta_x,
                           int32_t *not_pd, int32_t *min_bad_pivot);
 
+/* Inertia correction around the refactorization ("(delta_x, delta_c) are computed so as
+ * the regularized system satisfies (8)"; Cholesky success <=> In(K_k) = (n,0,0); for
+ * HyKKT the congruence of reading R9).  delta_c is not a parameter (reading R4).  Schedule
+ * (reading R15, from SPEC inertia_correction): per instance b, trial 0 with delta = 0; on
+ * NOT_PD the first nonzero delta is 1e-4 * max(1, ||W_b||_inf) (symmetric W, max row sum of |W_ij|)
+ * if delta_last[b] == 0, else max(1e-20, delta_last[b] / 3); each further failure multiplies delta
+ * by 8; a delta above 1e40 gives up on that instance.
+ *   Values as for ckkt_refactor.  delta_last [B] HOST (may be NULL = all 0): the previous IPM
+ *   iteration's accepted deltas.  delta_x [B] DEVICE, library-written: the deltas of the final
+ *   factorization; it stays referenced (zero-copy) like the value arrays until the last ckkt_solve.
+ *   delta_out [B], trials_out [B] HOST (may be NULL): accepted delta and number of factorizations
+ *   the instance needed (>= 1).  not_pd [B] DEVICE (may be NULL): final flags.
+ * Synchronous (one stream synchronisation per trial).  Every trial refactors the whole batch with
+ * the current per-instance deltas, so accepted instances are refactored to bit-identical factors.
+ * Returns CKKT_OK when every instance is positive definite, CKKT_NOT_PD when some instance gave up
+ * (its delta_out is the last delta tried), or the errors of ckkt_refactor. */
+ckkt_status ckkt_refactor_inertia(ckkt_ctx *ctx, const double *w_val, const double *g_val, const double *h_val,
+                                  const double *sigma_x, const double *d_s, const double *delta_last,
+                                  double *delta_x, double *delta_out, int32_t *trials_out, int32_t *not_pd);
+
 /* Newton step for the last refactorization: r1 [B,n], r2 [B,m_i], r3 [B,m_e], r4 [B,m_i] in;
  * dx [B,n], ds [B,m_i], dy [B,m_e], dz [B,m_i] out (device FP64; empty blocks may be NULL).
  * info: HOST array [B] or NULL.  With info != NULL the call synchronises the stream,

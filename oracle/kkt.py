@@ -232,7 +232,7 @@ def inertia_correction(kkt: SparseKKT, w_val, g_val, h_val, sigma_x, d_s, delta_
                        delta_first=1e-4, kappa_plus=8.0, delta_min=1e-20, delta_max=1e40):
     """Inertia correction around the refactorization ("(delta_x, delta_c) are computed so
     as the regularized system satisfies (8)"; Cholesky success <=> correct inertia).
-    Schedule = DESIGN.md reading R13 (SPEC inertia_correction): try delta = 0; on failure start at
+    Schedule = DESIGN.md reading R15 (SPEC inertia_correction): try delta = 0; on failure start at
     delta_first * max(1, ||W||_inf) if delta_last == 0, else max(delta_min, delta_last / 3) (kappa_minus = 1/3);
     multiply by kappa_plus after each further failure; give up above delta_max.
     Returns (delta, trials, failed)."""

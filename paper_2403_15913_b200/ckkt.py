@@ -20,6 +20,7 @@ CKKT_PATTERN_ERROR, CKKT_INVALID_ARG, CKKT_CUDA_ERROR, CKKT_OUT_OF_MEMORY = 4, 5
 CKKT_LIFTED, CKKT_HYKKT = 0, 1
 
 EXPORTED = ["ckkt_default_options", "ckkt_setup", "ckkt_get_sizes", "ckkt_export_symbolic", "ckkt_refactor",
+            "ckkt_refactor_inertia",
             "ckkt_solve", "ckkt_iterate_host", "ckkt_profile", "ckkt_phase_times", "ckkt_launch_count",
             "ckkt_destroy", "ckkt_status_str"]
 PHASES = ("condense", "factor", "forward", "backward", "vector")
@@ -79,6 +80,8 @@ def lib():
         L.ckkt_export_symbolic.restype = ctypes.c_int
         L.ckkt_refactor.argtypes = [P, P, P, P, P, P, P, P, P]
         L.ckkt_refactor.restype = ctypes.c_int
+        L.ckkt_refactor_inertia.argtypes = [P] * 11
+        L.ckkt_refactor_inertia.restype = ctypes.c_int
         L.ckkt_solve.argtypes = [P, P, P, P, P, P, P, P, P, ctypes.POINTER(ckkt_info)]
         L.ckkt_solve.restype = ctypes.c_int
         L.ckkt_iterate_host.argtypes = [P] * 16 + [ctypes.POINTER(ckkt_info)]
@@ -228,6 +231,19 @@ class Context:
                                  _dptr(delta_x), _dptr(not_pd), _dptr(min_bad_pivot))
         if rc:
             raise CKKTError(rc, "ckkt_refactor")
+
+    def refactor_inertia(self, w_val, g_val, h_val, sigma_x, d_s, delta_x, delta_last=None, not_pd=None):
+        """ckkt_refactor_inertia: delta_x is a device [B] FP64 tensor the library fills (keep it alive
+        until the last solve); returns (status, accepted deltas [B], trials [B]) as numpy arrays."""
+        dl = None if delta_last is None else np.ascontiguousarray(delta_last, dtype=np.float64)
+        dout = np.zeros(self.batch, np.float64)
+        tout = np.zeros(self.batch, np.int32)
+        rc = lib().ckkt_refactor_inertia(self.h, _dptr(w_val), _dptr(g_val), _dptr(h_val), _dptr(sigma_x),
+                                         _dptr(d_s), _hptr(dl), _dptr(delta_x), _hptr(dout), _hptr(tout),
+                                         _dptr(not_pd))
+        if rc not in (CKKT_OK, CKKT_NOT_PD):
+            raise CKKTError(rc, "ckkt_refactor_inertia")
+        return rc, dout, tout
 
     def solve(self, r1, r2, r3, r4, dx, ds, dy, dz, want_info: bool = True):
         infos = (ckkt_info * self.batch)() if want_info else None

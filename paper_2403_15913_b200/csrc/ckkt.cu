@@ -107,6 +107,48 @@ __global__ void k_gather_t(int64_t nnz, int B, const int32_t* __restrict__ e, co
   out[t] = val[b * nnz + e[k]];
 }
 
+// out[b][k] = val[b][e[k]] with separate strides (W values in the residual's symmetric internal-row
+// order), and sig[b][i] = sigma[b][perm2 i] + delta[b]: the residual then streams both contiguously
+__global__ void k_gather_ws(int64_t nnz_out, int64_t nnz_in, int B, const int32_t* __restrict__ e,
+                            const double* __restrict__ val, double* __restrict__ out) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= nnz_out * B) return;
+  const int64_t b = t / nnz_out, k = t - b * nnz_out;
+  out[t] = val[b * nnz_in + e[k]];
+}
+
+__global__ void k_gather_sigma(int n, const int32_t* __restrict__ perm2, const double* __restrict__ sigma,
+                               const double* __restrict__ delta, double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (i >= n) return;
+  out[(int64_t)b * n + i] = sigma[(int64_t)b * n + perm2[i]] + (delta ? delta[b] : 0.0);
+}
+
+// ||W||_inf per instance: max over rows of sum_j |W_ij| over the symmetric W (internal row order,
+// each row summed in its fixed entry order); block maxima + atomicMax on the bit patterns of
+// non-negative doubles (a maximum does not depend on the order: deterministic)
+__global__ void k_w_norminf(int n, const int32_t* __restrict__ ws_ptr, const double* __restrict__ wsv,
+                            int64_t ws_nnz, unsigned long long* __restrict__ out_bits) {
+  __shared__ double red[TPB / 32];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  double s = 0.0;
+  if (i < n) {
+    const double* w = wsv + b * ws_nnz;
+    for (int e = ws_ptr[i]; e < ws_ptr[i + 1]; ++e) s += fabs(w[e]);
+    if (s != s) s = INFINITY;
+  }
+  for (int o = 16; o > 0; o >>= 1) s = fmax(__shfl_down_sync(0xffffffffu, s, o), s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int k = 0; k < TPB / 32; ++k) t = fmax(red[k], t);
+    atomicMax(out_bits + b, (unsigned long long)__double_as_longlong(t));
+  }
+}
+
 __global__ void k_init_flags(int B, int* notpd, int* minpiv) {
   int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b < B) { notpd[b] = 0; minpiv[b] = INT_MAX; }
@@ -476,7 +518,9 @@ __global__ void k_recover(int mi, int n, const int32_t* __restrict__ rowptr, con
 struct ResArgs {
   int n, me, mi;
   const int32_t* perm2;
-  const int32_t *ws_ptr, *ws_col, *ws_idx;  // symmetric W (internal), entry -> w index
+  const int32_t *ws_ptr, *ws_col;  // symmetric W (internal rows)
+  const double *wsv, *sig;          // W values in that order; sigma + delta in internal order
+  int64_t ws_nnz;
   const int32_t *gt_ptr, *gt_e, *gt_r, *ht_ptr, *ht_e, *ht_r;
   const int32_t *g_rowptr, *g_col2, *h_rowptr, *h_col2;
   const double *w_val, *g_val, *h_val, *sigma, *d_s, *delta;
@@ -494,15 +538,15 @@ __device__ __forceinline__ void kaug_residual_row(const ResArgs& a, int b, int64
   if (t < n) {
     const int i = (int)t;
     const int oi = a.perm2[i];
-    const double* w = a.w_val + b * a.w_nnz;
+    const double* w = a.wsv + b * a.ws_nnz;
     const double* dx = a.dx + (int64_t)b * n;
     double acc = 0.0, aa = 0.0;
     for (int e = a.ws_ptr[i]; e < a.ws_ptr[i + 1]; ++e) {
-      double v = w[a.ws_idx[e]] * dx[a.ws_col[e]];
+      double v = w[e] * dx[a.ws_col[e]];
       acc += v;
       aa += fabs(v);
     }
-    double dg = (a.sigma[(int64_t)b * n + oi] + (a.delta ? a.delta[b] : 0.0)) * dx[i];
+    double dg = a.sig[(int64_t)b * n + i] * dx[i];
     acc += dg;
     aa += fabs(dg);
     if (me) {
@@ -672,6 +716,8 @@ struct ckkt_ctx {
   int32_t *gt_ptr = nullptr, *gt_e = nullptr, *gt_r = nullptr, *ht_ptr = nullptr, *ht_e = nullptr, *ht_r = nullptr;
   int32_t *g_rowptr = nullptr, *g_col2 = nullptr, *h_rowptr = nullptr, *h_col2 = nullptr;
   int32_t *ws_ptr = nullptr, *ws_col = nullptr, *ws_idx = nullptr;
+  int64_t ws_nnz = 0;
+  double *wsv = nullptr, *sig_i = nullptr;  // residual copies (symmetric internal W order; sigma+delta internal)
   // numeric
   double *Kval = nullptr, *L = nullptr, *Ub = nullptr, *Vb = nullptr;
   int64_t Usize = 0, Vsize = 0;
@@ -727,7 +773,7 @@ struct ckkt_ctx {
   double *cds = nullptr, *cdy = nullptr, *cdz = nullptr;          // correction blocks
   double *rho1 = nullptr, *rho2 = nullptr, *rho3 = nullptr, *rho4 = nullptr;
   double *rho1b = nullptr, *rho2b = nullptr, *rho3b = nullptr, *rho4b = nullptr;
-  double *part = nullptr, *omega = nullptr, *resinf = nullptr;
+  double *part = nullptr, *omega = nullptr, *resinf = nullptr, *wnorm_dev = nullptr;
   double *cg_rr = nullptr, *cg_bn = nullptr, *cg_alpha = nullptr, *cg_beta = nullptr;
   int *cg_done = nullptr, *cg_iters = nullptr, *active = nullptr, *accflag = nullptr, *skipflag = nullptr;
   int* h_pinned_int = nullptr;
@@ -1087,6 +1133,7 @@ ckkt_status setup_device(ckkt_ctx* c) {
     UP(c->ws_ptr, ptr);
     UP(c->ws_col, col);
     UP(c->ws_idx, idx);
+    c->ws_nnz = (int64_t)ent.size();
   }
 #undef UP
   DALLOC(c->Kval, (size_t)B * c->nnzk);
@@ -1097,6 +1144,8 @@ ckkt_status setup_device(ckkt_ctx* c) {
   CK(cudaMemset(c->epoch_dev, 0, 2 * sizeof(int)));
   DALLOC(c->gtv, (size_t)B * std::max<int64_t>(c->g_nnz, 1));
   DALLOC(c->htv, (size_t)B * std::max<int64_t>(c->h_nnz, 1));
+  DALLOC(c->wsv, (size_t)B * std::max<int64_t>(c->ws_nnz, 1));
+  DALLOC(c->sig_i, (size_t)B * n);
   DALLOC(c->notpd, B);
   DALLOC(c->minpiv, B);
   const size_t Bn = (size_t)B * n, Bme = (size_t)B * std::max(me, 1), Bmi = (size_t)B * std::max(mi, 1);
@@ -1128,6 +1177,7 @@ ckkt_status setup_device(ckkt_ctx* c) {
   DALLOC(c->part, (size_t)B * 1024);
   DALLOC(c->omega, 2 * B);
   DALLOC(c->resinf, 2 * B);
+  DALLOC(c->wnorm_dev, B);
   DALLOC(c->cg_rr, B);
   DALLOC(c->cg_bn, B);
   DALLOC(c->cg_alpha, B);
@@ -1357,6 +1407,13 @@ ckkt_status ckkt_refactor(ckkt_ctx* c, const double* w_val, const double* g_val,
     k_gather_t<<<(unsigned)((c->h_nnz * B + TPB - 1) / TPB), TPB, 0, st>>>(c->h_nnz, B, c->ht_e, h_val, c->htv);
     c->launches++;
   }
+  if (c->ws_nnz) {
+    k_gather_ws<<<(unsigned)((c->ws_nnz * B + TPB - 1) / TPB), TPB, 0, st>>>(c->ws_nnz, c->w_nnz, B, c->ws_idx, w_val,
+                                                                          c->wsv);
+    c->launches++;
+  }
+  k_gather_sigma<<<dim3(nblk(c->n), B), TPB, 0, st>>>(c->n, c->S.perm2, sigma_x, delta_x, c->sig_i);
+  c->launches++;
   k_init_flags<<<nblk(B), TPB, 0, st>>>(B, c->notpd, c->minpiv);
   prof_begin(c, 0);
   {
@@ -1403,6 +1460,63 @@ ckkt_status ckkt_refactor(ckkt_ctx* c, const double* w_val, const double* g_val,
   CK(cudaGetLastError());
   c->factored = true;
   return CKKT_OK;
+}
+
+
+// Inertia correction around the refactorization (reading R15 of DESIGN.md,
+// schedule of SPEC inertia_correction).  Per instance: trial 0 uses delta = 0; on NOT_PD the first
+// nonzero delta is 1e-4 * max(1, ||W||_inf) when delta_last == 0, else max(1e-20, delta_last / 3);
+// every further failure multiplies it by 8; delta > 1e40 gives up (instance stays NOT_PD).  Every
+// trial refactors the whole batch with the current per-instance deltas (accepted instances keep
+// theirs, so their factors are recomputed bit-identically).
+ckkt_status ckkt_refactor_inertia(ckkt_ctx* c, const double* w_val, const double* g_val, const double* h_val,
+                                  const double* sigma_x, const double* d_s, const double* delta_last,
+                                  double* delta_x, double* delta_out, int32_t* trials_out, int32_t* not_pd) {
+  if (!c || !c->has_device || !delta_x) return CKKT_INVALID_ARG;
+  const int B = c->B;
+  cudaStream_t st = c->stream;
+  std::vector<double> delta(B, 0.0), wnorm(B, -1.0);
+  std::vector<int32_t> trials(B, 0), flag(B, 0), done(B, 0);
+  ckkt_status rs = CKKT_OK;
+  for (;;) {
+    CK(cudaMemcpyAsync(delta_x, delta.data(), sizeof(double) * B, cudaMemcpyHostToDevice, st));
+    ckkt_status s = ckkt_refactor(c, w_val, g_val, h_val, sigma_x, d_s, delta_x, nullptr, nullptr);
+    if (s != CKKT_OK) return s;
+    if (wnorm[0] < 0.0) {  // once: ||W||_inf from the residual's symmetric W copy (gathered by the refactor)
+      unsigned long long* nb = reinterpret_cast<unsigned long long*>(c->wnorm_dev);
+      CK(cudaMemsetAsync(nb, 0, sizeof(double) * B, st));
+      if (c->ws_nnz) {
+        k_w_norminf<<<dim3(nblk(c->n), B), TPB, 0, st>>>(c->n, c->ws_ptr, c->wsv, c->ws_nnz, nb);
+        c->launches++;
+      }
+      CK(cudaMemcpyAsync(wnorm.data(), nb, sizeof(double) * B, cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaMemcpyAsync(flag.data(), c->notpd, sizeof(int32_t) * B, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    bool again = false;
+    for (int b = 0; b < B; ++b) {
+      if (done[b]) continue;
+      trials[b]++;
+      if (!flag[b]) { done[b] = 1; continue; }
+      double d;
+      if (delta[b] == 0.0) {
+        const double last = delta_last ? delta_last[b] : 0.0;
+        d = (last == 0.0) ? 1e-4 * std::max(1.0, wnorm[b]) : std::max(1e-20, last / 3.0);
+      } else {
+        d = 8.0 * delta[b];
+      }
+      if (!(d <= 1e40)) { done[b] = 2; continue; }  // StrategyFailure: keep the last (failed) delta
+      delta[b] = d;
+      again = true;
+    }
+    if (!again) break;
+  }
+  for (int b = 0; b < B; ++b)
+    if (done[b] == 2) rs = CKKT_NOT_PD;
+  if (not_pd) CK(cudaMemcpyAsync(not_pd, c->notpd, sizeof(int32_t) * B, cudaMemcpyDeviceToDevice, st));
+  if (delta_out) std::copy(delta.begin(), delta.end(), delta_out);
+  if (trials_out) std::copy(trials.begin(), trials.end(), trials_out);
+  return rs;
 }
 
 }  // extern "C"
@@ -1665,7 +1779,7 @@ void residual(ckkt_ctx* c, const double* r1, const double* r2, const double* r3,
   ResArgs a;
   a.n = n; a.me = me; a.mi = mi;
   a.perm2 = c->S.perm2;
-  a.ws_ptr = c->ws_ptr; a.ws_col = c->ws_col; a.ws_idx = c->ws_idx;
+  a.ws_ptr = c->ws_ptr; a.ws_col = c->ws_col; a.wsv = c->wsv; a.sig = c->sig_i; a.ws_nnz = c->ws_nnz;
   a.gt_ptr = c->gt_ptr; a.gt_e = c->gt_e; a.gt_r = c->gt_r;
   a.ht_ptr = c->ht_ptr; a.ht_e = c->ht_e; a.ht_r = c->ht_r;
   a.g_rowptr = c->g_rowptr; a.g_col2 = c->g_col2; a.h_rowptr = c->h_rowptr; a.h_col2 = c->h_col2;

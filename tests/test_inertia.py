@@ -1,4 +1,4 @@
-"""Inertia correction (reading R13): the oracle's delta_x search
+"""Inertia correction (reading R15): the oracle's delta_x search
 pinned to closed forms and to dense eigenvalues, and the C-ABI ckkt_refactor_inertia against it."""
 from __future__ import annotations
 
