@@ -268,3 +268,15 @@ def _gather_csr(K, rows, cols):
     hit = (pos < len(kkey)) & (kkey[pos_c] == key)
     out[hit] = data[pos_c[hit]]
     return out
+
+
+def fraction_to_boundary(s, ds, tau):
+    """Largest alpha in (0, 1] with s + alpha ds >= (1 - tau) s, for s > 0 (the step
+    length is "computed using a fraction-to-boundary rule"; SPEC fraction_to_boundary):
+    alpha = min(1, min over ds_i < 0 of tau s_i / (-ds_i)).  Entries whose ratio is NaN are
+    skipped (Python's min keeps the running value against NaN)."""
+    alpha = 1.0
+    for si, di in zip(np.asarray(s, dtype=np.float64).tolist(), np.asarray(ds, dtype=np.float64).tolist()):
+        if di < 0:
+            alpha = min(alpha, tau * si / -di)
+    return alpha
