@@ -159,6 +159,16 @@ ckkt_status ckkt_refactor_inertia(ckkt_ctx *ctx, const double *w_val, const doub
                                   const double *sigma_x, const double *d_s, const double *delta_last,
                                   double *delta_x, double *delta_out, int32_t *trials_out, int32_t *not_pd);
 
+/* Fraction-to-boundary rule ("computed using a fraction-to-boundary rule"; SPEC
+ * fraction_to_boundary): for each of `batch` instances, the largest alpha in (0, 1] with
+ * s + alpha ds >= (1 - tau) s, i.e. alpha[b] = min(1, min over ds_i < 0 of (tau s_i) / (-ds_i)).
+ *   s, ds [batch, len] DEVICE FP64 (s > 0 is the caller's precondition); 0 < tau < 1;
+ *   alpha [batch] DEVICE FP64 out; stream = cudaStream_t (NULL = default stream).  Entries whose
+ *   ratio is NaN are skipped.  Asynchronous, stateless (no context), deterministic (bit-exact).
+ * Returns CKKT_INVALID_ARG for tau outside (0, 1), negative sizes or missing pointers. */
+ckkt_status ckkt_fraction_to_boundary(int32_t batch, int64_t len, const double *s, const double *ds, double tau,
+                                      double *alpha, void *stream);
+
 /* Newton step for the last refactorization: r1 [B,n], r2 [B,m_i], r3 [B,m_e], r4 [B,m_i] in;
  * dx [B,n], ds [B,m_i], dy [B,m_e], dz [B,m_i] out (device FP64; empty blocks may be NULL).
  * info: HOST array [B] or NULL.  With info != NULL the call synchronises the stream,

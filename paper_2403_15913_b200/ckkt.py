@@ -20,7 +20,7 @@ CKKT_PATTERN_ERROR, CKKT_INVALID_ARG, CKKT_CUDA_ERROR, CKKT_OUT_OF_MEMORY = 4, 5
 CKKT_LIFTED, CKKT_HYKKT = 0, 1
 
 EXPORTED = ["ckkt_default_options", "ckkt_setup", "ckkt_get_sizes", "ckkt_export_symbolic", "ckkt_refactor",
-            "ckkt_refactor_inertia",
+            "ckkt_refactor_inertia", "ckkt_fraction_to_boundary",
             "ckkt_solve", "ckkt_iterate_host", "ckkt_profile", "ckkt_phase_times", "ckkt_launch_count",
             "ckkt_destroy", "ckkt_status_str"]
 PHASES = ("condense", "factor", "forward", "backward", "vector")
@@ -82,6 +82,8 @@ def lib():
         L.ckkt_refactor.restype = ctypes.c_int
         L.ckkt_refactor_inertia.argtypes = [P] * 11
         L.ckkt_refactor_inertia.restype = ctypes.c_int
+        L.ckkt_fraction_to_boundary.argtypes = [ctypes.c_int32, ctypes.c_int64, P, P, ctypes.c_double, P, P]
+        L.ckkt_fraction_to_boundary.restype = ctypes.c_int
         L.ckkt_solve.argtypes = [P, P, P, P, P, P, P, P, P, ctypes.POINTER(ckkt_info)]
         L.ckkt_solve.restype = ctypes.c_int
         L.ckkt_iterate_host.argtypes = [P] * 16 + [ctypes.POINTER(ckkt_info)]
@@ -98,6 +100,23 @@ def lib():
         L.ckkt_status_str.restype = ctypes.c_char_p
         _lib = L
     return _lib
+
+
+def fraction_to_boundary(s, ds, tau: float):
+    """ckkt_fraction_to_boundary on [B, len] (or [len]) device FP64 tensors; returns alpha [B] on the device,
+    enqueued on torch's current stream."""
+    import torch
+    if s.shape != ds.shape or s.dtype != torch.float64 or ds.dtype != torch.float64:
+        raise ValueError("s and ds: same shape, float64")
+    if s.dim() not in (1, 2):
+        raise ValueError("s and ds: [len] or [B, len]")
+    s2, d2 = (s, ds) if s.dim() == 2 else (s.unsqueeze(0), ds.unsqueeze(0))
+    alpha = torch.empty(s2.shape[0], dtype=torch.float64, device=s.device)
+    rc = lib().ckkt_fraction_to_boundary(s2.shape[0], s2.shape[1], _dptr(s2), _dptr(d2), float(tau), _dptr(alpha),
+                                         ctypes.c_void_p(torch.cuda.current_stream(s.device).cuda_stream))
+    if rc:
+        raise CKKTError(rc, "ckkt_fraction_to_boundary")
+    return alpha
 
 
 class CKKTError(RuntimeError):

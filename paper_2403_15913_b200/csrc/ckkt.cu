@@ -149,6 +149,39 @@ __global__ void k_w_norminf(int n, const int32_t* __restrict__ ws_ptr, const dou
   }
 }
 
+// fraction-to-boundary: alpha[b] = min(1, min over ds < 0 of (tau s) / (-ds)).  Grid-stride
+// per instance (blockIdx.y), block minimum, then atomicMin on the bit patterns of the (non-negative)
+// ratios: a minimum is order independent, so the result is bit-exact.  NaN ratios are skipped.
+__global__ void k_ftb_init(int B, double* __restrict__ alpha) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < B) alpha[b] = 1.0;
+}
+
+__global__ void k_ftb(int64_t len, const double* __restrict__ s, const double* __restrict__ ds, double tau,
+                      unsigned long long* __restrict__ alpha_bits) {
+  __shared__ double red[TPB / 32];
+  const int64_t b = blockIdx.y;
+  double m = 1.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) {
+    const double d = ds[b * len + i];
+    if (d < 0.0) {
+      const double r = (tau * s[b * len + i]) / (-d);
+      if (r < m) m = r;  // false for NaN
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double t = __shfl_down_sync(0xffffffffu, m, o);
+    if (t < m) m = t;
+  }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < TPB / 32; ++k)  // red[0] is this warp's own minimum
+      if (red[k] < m) m = red[k];
+    if (m < 1.0) atomicMin(alpha_bits + b, (unsigned long long)__double_as_longlong(m));
+  }
+}
+
 __global__ void k_init_flags(int B, int* notpd, int* minpiv) {
   int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b < B) { notpd[b] = 0; minpiv[b] = INT_MAX; }
@@ -1517,6 +1550,22 @@ ckkt_status ckkt_refactor_inertia(ckkt_ctx* c, const double* w_val, const double
   if (delta_out) std::copy(delta.begin(), delta.end(), delta_out);
   if (trials_out) std::copy(trials.begin(), trials.end(), trials_out);
   return rs;
+}
+
+
+ckkt_status ckkt_fraction_to_boundary(int32_t batch, int64_t len, const double* s, const double* ds, double tau,
+                                      double* alpha, void* stream) {
+  if (batch < 0 || len < 0 || !(tau > 0.0 && tau < 1.0) || (batch > 0 && (!alpha || (len > 0 && (!s || !ds)))))
+    return CKKT_INVALID_ARG;
+  if (batch == 0) return CKKT_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  k_ftb_init<<<nblk(batch), TPB, 0, st>>>(batch, alpha);
+  if (len > 0) {
+    const unsigned gx = (unsigned)std::min<int64_t>(nblk(len), 4 * 148);
+    k_ftb<<<dim3(gx, batch), TPB, 0, st>>>(len, s, ds, tau, reinterpret_cast<unsigned long long*>(alpha));
+  }
+  CK(cudaGetLastError());
+  return CKKT_OK;
 }
 
 }  // extern "C"
