@@ -494,3 +494,41 @@ class Instance:
 
 def random_rhs(n: int, seed: int) -> np.ndarray:
     return np.random.default_rng(seed).standard_normal(n)
+
+
+class NLP:
+    """The (gradient-scaled, reading R14) distillation NLP of one instance as the callbacks the IPM
+    driver (paper_2403_15913_b200/ipm.py) needs: min s_f f(v) s.t. S_r c(v) = 0, u_lo <= u <= u_hi."""
+
+    def __init__(self, inst: "Instance"):
+        from scipy.sparse import csr_matrix
+        md = inst.model
+        self.inst, self.md = inst, md
+        self.n, self.m = md.n, md.m
+        self.pat = md.pat
+        self.bidx = np.arange(md.N + 1) * NV + OU
+        self.lo = np.full(md.N + 1, md.p.u_lo)
+        self.hi = np.full(md.N + 1, md.p.u_hi)
+        self.x0 = inst.v.copy()
+        self.lam0 = inst.lam.copy()
+        self.sf, self.rs = inst.obj_scale, inst.row_scale
+        self._rse = inst.row_scale[inst.rows_of_entries]
+        self._csr = lambda jv: csr_matrix((jv, self.pat.j_col, self.pat.j_rowptr), shape=(md.m, md.n))
+
+    def f(self, v):
+        return self.sf * self.md.objective(v)
+
+    def grad_f(self, v):
+        return self.sf * self.md.grad_f(v)
+
+    def c(self, v):
+        return self.rs * self.md.residual(v, self.inst.xbar0)
+
+    def jac(self, v):
+        return self.md.jacobian_values(v) * self._rse
+
+    def jac_t(self, v, jv, y):
+        return self._csr(jv).T @ y
+
+    def hess(self, v, lam):
+        return self.md.hessian_values(v, lam * self.rs, self.sf)

@@ -1,0 +1,185 @@
+"""Interior-point loop around the C ABI (host driver, not the hot path).
+
+The paper runs MadNLP's filter line-search interior-point method ([17] = Wächter and
+Biegler) with the condensed-KKT Newton step on the GPU.  This module is that loop for NLPs of the
+form  min f(v)  s.t.  c(v) = 0,  lo <= v_B <= hi  (bounds on a subset B of the variables),
+with the per-iteration linear algebra entirely in libckkt (HyKKT, m_e = m, m_i = 0):
+
+  * inertia correction: ckkt_refactor_inertia (reading R15);
+  * Newton step: ckkt_solve of  [W + Sigma_x + delta_x I, J^T; J, 0] [dx; dlam] = -[r1; r3]  with
+    r1 = grad f + J^T lam - mu/(v_B - lo) + mu/(hi - v_B)  (primal-dual barrier gradient)
+    and Sigma_x = z_L/(v_B - lo) + z_U/(hi - v_B);
+  * step lengths: ckkt_fraction_to_boundary on the bound slacks and on the bound duals (tau =
+    max(0.99, 1 - mu));
+  * line search: the Wächter–Biegler filter (switching condition, Armijo on the barrier objective,
+    sufficient decrease of theta = ||c||_1 or phi, filter augmentation), without second-order
+    corrections or feasibility restoration (a step below alpha_min stops with status "restoration");
+  * barrier update (SPEC update_mu): mu' = max(tol/10, min(0.2 mu, mu^1.5)) once
+    E_mu <= 10 mu; stop when E_0 <= tol (tol = 1e-6).
+
+Host arithmetic here is O(n) vector bookkeeping in numpy on iterates copied back from the device;
+the model evaluation (f, c, J, W) is the caller's `problem` (ExaModels AD is out of scope, §8(f) 4).
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+
+import numpy as np
+
+# Wächter–Biegler constants ([17], Ipopt defaults)
+GAMMA_THETA, GAMMA_PHI, DELTA_SW, S_THETA, S_PHI, ETA_PHI = 1e-5, 1e-5, 1.0, 1.1, 2.3, 1e-4
+KAPPA_EPS, KAPPA_MU, THETA_MU, KAPPA_SIGMA = 10.0, 0.2, 1.5, 1e10
+
+
+@dataclasses.dataclass
+class IPMResult:
+    status: str                 # "converged" | "max_iter" | "restoration" | "inertia_failure"
+    iterations: int
+    v: np.ndarray
+    lam: np.ndarray
+    z_lo: np.ndarray
+    z_hi: np.ndarray
+    objective: float
+    kkt_error: float
+    history: list               # per iteration: dict(mu, theta, phi, alpha, delta_x, k_cg, trials, ls)
+
+
+class GpuKKT:
+    """The per-iteration solve through libckkt (HyKKT).  refactor(w, j, sigma, delta_last) ->
+    (ok, delta, trials); solve(r1, r3) -> (dx, dlam, info)."""
+
+    def __init__(self, n, m, w_row, w_col, j_rowptr, j_col, gamma=1e7, leaf=64, device=0):
+        import torch
+        from . import ckkt
+        self.torch, self.ckkt = torch, ckkt
+        self.dev = torch.device("cuda", device)
+        self.n, self.m = n, m
+        self.ctx = ckkt.Context(n, m, 0, w_row, w_col, j_rowptr, j_col, None, None, strategy=ckkt.CKKT_HYKKT,
+                                gamma=gamma, leaf=leaf, device=device,
+                                stream=torch.cuda.current_stream(self.dev).cuda_stream)
+        self.delta = torch.zeros(1, dtype=torch.float64, device=self.dev)
+
+    def _t(self, a):
+        return self.torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64), device=self.dev)
+
+    def refactor(self, w_val, j_val, sigma_x, delta_last):
+        self._vals = [self._t(w_val), self._t(j_val), None, self._t(sigma_x), None]  # zero-copy: keep alive
+        rc, d, t = self.ctx.refactor_inertia(*self._vals, self.delta, np.array([delta_last]))
+        return rc == self.ckkt.CKKT_OK, float(d[0]), int(t[0])
+
+    def solve(self, r1, r3):
+        T = self.torch
+        dx = T.empty(self.n, dtype=T.float64, device=self.dev)
+        dy = T.empty(self.m, dtype=T.float64, device=self.dev)
+        rc, info = self.ctx.solve(self._t(r1), None, self._t(r3), None, dx, None, dy, None)
+        return dx.cpu().numpy(), dy.cpu().numpy(), info[0]
+
+    def fraction_to_boundary(self, s, ds, tau):
+        a = self.ckkt.fraction_to_boundary(self._t(s), self._t(ds), tau)
+        return float(a.cpu().numpy()[0])
+
+
+def solve_nlp(problem, kkt, mu0=0.1, tol=1e-6, max_iter=200, alpha_min_frac=0.05, verbose=False) -> IPMResult:
+    """Filter line-search IPM (see the module docstring).  `problem` provides n, m, bidx (indices of
+    the bounded variables), lo, hi, x0, lam0, f(v), grad_f(v), c(v), jac(v) (J values in the
+    pattern's CSR order), jac_t(v, jv, y) (J^T y), jac_mul(jv, d) (J d) and hess(v, lam) (W values
+    of f + lam^T c).  `kkt` provides refactor / solve / fraction_to_boundary (GpuKKT)."""
+    P = problem
+    b, lo, hi = P.bidx, P.lo, P.hi
+    v = P.x0.copy()
+    lam = P.lam0.copy()
+    mu = mu0
+    sl, su = v[b] - lo, hi - v[b]
+    z_lo, z_hi = mu / sl, mu / su
+    delta_last = 0.0
+    hist = []
+
+    def barrier(vv, mu_):
+        return P.f(vv) - mu_ * (np.log(vv[b] - lo).sum() + np.log(hi - vv[b]).sum())
+
+    def kkt_error(vv, ll, zl, zu, jv, mu_):
+        g = P.grad_f(vv) + P.jac_t(vv, jv, ll)
+        g[b] += -zl + zu
+        comp = max(np.abs((vv[b] - lo) * zl - mu_).max(initial=0.0), np.abs((hi - vv[b]) * zu - mu_).max(initial=0.0))
+        return max(np.abs(g).max(initial=0.0), np.abs(P.c(vv)).max(initial=0.0), comp)
+
+    cv = P.c(v)
+    theta0 = np.abs(cv).sum()
+    theta_max, theta_min = 1e4 * max(1.0, theta0), 1e-4 * max(1.0, theta0)
+    filt = []
+    status = "max_iter"
+    it = 0
+    for it in range(max_iter + 1):
+        jv = P.jac(v)
+        err0 = kkt_error(v, lam, z_lo, z_hi, jv, 0.0)
+        if err0 <= tol:
+            status = "converged"
+            break
+        while kkt_error(v, lam, z_lo, z_hi, jv, mu) <= KAPPA_EPS * mu and mu > tol / 10 * (1 + 1e-12):
+            mu = max(tol / 10, min(KAPPA_MU * mu, mu ** THETA_MU))   # SPEC update_mu
+            filt = []
+        if it == max_iter:
+            break
+        sl, su = v[b] - lo, hi - v[b]
+        sigma = np.zeros(P.n)
+        sigma[b] = z_lo / sl + z_hi / su
+        ok, delta, trials = kkt.refactor(P.hess(v, lam), jv, sigma, delta_last)
+        if not ok:
+            status = "inertia_failure"
+            break
+        if delta > 0:
+            delta_last = delta
+        r1 = P.grad_f(v) + P.jac_t(v, jv, lam)
+        r1[b] += -mu / sl + mu / su
+        cv = P.c(v)
+        dx, dlam, info = kkt.solve(r1, cv)
+        dzl = mu / sl - z_lo - (z_lo / sl) * dx[b]
+        dzu = mu / su - z_hi + (z_hi / su) * dx[b]
+        tau = max(0.99, 1.0 - mu)
+        a_max = min(kkt.fraction_to_boundary(np.concatenate([sl, su]), np.concatenate([dx[b], -dx[b]]), tau), 1.0)
+        a_z = kkt.fraction_to_boundary(np.concatenate([z_lo, z_hi]), np.concatenate([dzl, dzu]), tau)
+        # ---- filter line search (Wächter–Biegler)
+        theta = np.abs(cv).sum()
+        phi = barrier(v, mu)
+        gphi = P.grad_f(v)
+        gphi[b] += -mu / sl + mu / su
+        dphi = float(gphi @ dx)
+        alpha, ls, accepted, armijo = a_max, 0, False, False
+        a_lo = alpha_min_frac * a_max * min(GAMMA_THETA, GAMMA_PHI * theta / max(-dphi, 1e-300)) if dphi < 0 \
+            else alpha_min_frac * a_max * GAMMA_THETA
+        while alpha >= a_lo and alpha > 1e-16:
+            vt = v + alpha * dx
+            tt = np.abs(P.c(vt)).sum()
+            pt = barrier(vt, mu)
+            if math.isfinite(pt) and tt <= theta_max and not any(tt >= ft and pt >= fp for ft, fp in filt):
+                switching = dphi < 0 and alpha * (-dphi) ** S_PHI > DELTA_SW * theta ** S_THETA
+                if theta <= theta_min and switching:
+                    if pt <= phi + ETA_PHI * alpha * dphi:
+                        accepted, armijo = True, True
+                elif tt <= (1 - GAMMA_THETA) * theta or pt <= phi - GAMMA_PHI * theta:
+                    accepted = True
+            if accepted:
+                break
+            alpha *= 0.5
+            ls += 1
+        if not accepted:
+            status = "restoration"
+            break
+        if not armijo:
+            filt.append(((1 - GAMMA_THETA) * theta, phi - GAMMA_PHI * theta))
+        v = v + alpha * dx
+        lam = lam + alpha * dlam
+        z_lo = z_lo + a_z * dzl
+        z_hi = z_hi + a_z * dzu
+        # keep the bound duals within KAPPA_SIGMA of mu / slack (Ipopt's safeguard)
+        sl, su = v[b] - lo, hi - v[b]
+        z_lo = np.clip(z_lo, mu / (KAPPA_SIGMA * sl), KAPPA_SIGMA * mu / sl)
+        z_hi = np.clip(z_hi, mu / (KAPPA_SIGMA * su), KAPPA_SIGMA * mu / su)
+        hist.append(dict(mu=mu, theta=theta, phi=phi, alpha=alpha, alpha_z=a_z, delta_x=delta, trials=trials,
+                         k_cg=int(info.get("k_cg", 0)) if isinstance(info, dict) else 0, ls=ls))
+        if verbose:
+            print(f"it {it:3d} mu {mu:.2e} theta {theta:.2e} phi {phi:.6e} alpha {alpha:.3e} delta {delta:.1e} "
+                  f"ls {ls}")
+    return IPMResult(status=status, iterations=it, v=v, lam=lam, z_lo=z_lo, z_hi=z_hi, objective=P.f(v),
+                     kkt_error=kkt_error(v, lam, z_lo, z_hi, P.jac(v), 0.0), history=hist)

@@ -1,0 +1,130 @@
+"""IPM loop around the ABI (paper_2403_15913_b200/ipm.py): host logic on CPU
+with the oracle as the linear solver, and on the GPU through libckkt with iteration parity against
+the oracle-driven run (HyKKT reaches the iteration counts of an exact factorization)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from inputs import distillation as dist
+from kkt_cases import E32
+from oracle import kkt as K
+from paper_2403_15913_b200 import ipm
+
+
+class OracleKKT:
+    """Test adapter: the same refactor / solve / fraction_to_boundary calls served by the oracle."""
+
+    def __init__(self, nlp, gamma=1e7):
+        p = nlp.pat
+        self.o = K.SparseKKT(nlp.n, nlp.m, 0, p.w_row, p.w_col, p.j_rowptr, p.j_col, E32, E32[:0],
+                             strategy=K.HYKKT, gamma=gamma, leaf=64)
+
+    def refactor(self, w_val, j_val, sigma_x, delta_last):
+        d, t, failed = K.inertia_correction(self.o, w_val, j_val, [], sigma_x, [], delta_last=delta_last)
+        return not failed, d, t
+
+    def solve(self, r1, r3):
+        (dx, ds, dy, dz), info = self.o.solve(r1, np.zeros(0), r3, np.zeros(0))
+        return dx, dy, {"k_cg": info.k_cg}
+
+    def fraction_to_boundary(self, s, ds, tau):
+        return K.fraction_to_boundary(s, ds, tau)
+
+
+class _Pat:
+    def __init__(self, w_row, w_col, j_rowptr, j_col):
+        self.w_row, self.w_col = np.asarray(w_row, np.int32), np.asarray(w_col, np.int32)
+        self.j_rowptr, self.j_col = np.asarray(j_rowptr, np.int32), np.asarray(j_col, np.int32)
+
+
+class RosenNLP:
+    """Nonconvex toy: min (1-x)^2 + 100 (y - x^2)^2 + (u - 2)^2  s.t.  x - u + 1 = 0,  1 <= u <= 5.
+    Optimum (1, 1, 2), f = 0.  From (0.5, 1.5, 1.5) the reduced Hessian is indefinite, so the loop
+    needs the inertia correction (delta_x > 0) and the line search backtracks."""
+    n, m = 3, 1
+    pat = _Pat([0, 1, 1, 2], [0, 0, 1, 2], [0, 2], [0, 2])
+    bidx = np.array([2])
+    lo, hi = np.array([1.0]), np.array([5.0])
+
+    def __init__(self):
+        self.x0 = np.array([0.5, 1.5, 1.5])
+        self.lam0 = np.zeros(1)
+
+    def f(self, v):
+        x, y, u = v
+        return (1 - x) ** 2 + 100 * (y - x * x) ** 2 + (u - 2) ** 2
+
+    def grad_f(self, v):
+        x, y, u = v
+        return np.array([-2 * (1 - x) - 400 * x * (y - x * x), 200 * (y - x * x), 2 * (u - 2)])
+
+    def c(self, v):
+        return np.array([v[0] - v[2] + 1])
+
+    def jac(self, v):
+        return np.array([1.0, -1.0])
+
+    def jac_t(self, v, jv, y):
+        return np.array([jv[0] * y[0], 0.0, jv[1] * y[0]])
+
+    def hess(self, v, lam):
+        x, y, u = v
+        return np.array([2 - 400 * y + 1200 * x * x, -400 * x, 200.0, 2.0])
+
+
+def test_ipm_oracle_nonconvex_uses_inertia_correction():
+    nlp = RosenNLP()
+    res = ipm.solve_nlp(nlp, OracleKKT(nlp), max_iter=100)
+    assert res.status == "converged", res
+    assert np.allclose(res.v, [1.0, 1.0, 2.0], atol=1e-5)
+    assert any(h["delta_x"] > 0 for h in res.history)
+    assert any(h["trials"] > 1 for h in res.history)
+
+
+@pytest.mark.gpu
+def test_ipm_gpu_nonconvex_parity():
+    """The nonconvex toy through libckkt: same iterations, deltas and trial counts as the oracle."""
+    r_o = ipm.solve_nlp(RosenNLP(), OracleKKT(RosenNLP()), max_iter=100)
+    p = RosenNLP.pat
+    r_g = ipm.solve_nlp(RosenNLP(), ipm.GpuKKT(3, 1, p.w_row, p.w_col, p.j_rowptr, p.j_col, leaf=4), max_iter=100)
+    assert r_g.status == r_o.status == "converged"
+    assert r_g.iterations == r_o.iterations
+    assert [h["trials"] for h in r_g.history] == [h["trials"] for h in r_o.history]
+    np.testing.assert_allclose([h["delta_x"] for h in r_g.history], [h["delta_x"] for h in r_o.history], rtol=1e-12)
+    assert np.abs(r_g.v - r_o.v).max() <= 1e-8
+
+
+def _check_solution(nlp, res):
+    assert res.status == "converged", (res.status, res.iterations)
+    assert res.kkt_error <= 1e-6
+    assert np.abs(nlp.c(res.v)).max() <= 1e-6
+    u = res.v[nlp.bidx]
+    assert np.all(u > nlp.lo) and np.all(u < nlp.hi)
+
+
+def test_ipm_oracle_converges_distillation():
+    """Host logic: the filter line-search IPM converges on the N = 4 distillation NLP to tol 1e-6
+     from the simulated start, with bound multipliers >= 0 and u strictly inside its bounds."""
+    nlp = dist.NLP(dist.Instance(4))
+    res = ipm.solve_nlp(nlp, OracleKKT(nlp), max_iter=100)
+    _check_solution(nlp, res)
+    assert np.all(res.z_lo > 0) and np.all(res.z_hi > 0)
+    assert res.history[-1]["mu"] <= 1e-6
+
+
+@pytest.mark.gpu
+def test_ipm_gpu_iteration_parity():
+    """The same IPM with the libckkt HyKKT solve (inertia correction and fraction-to-boundary on
+    the device) converges on N = 10 in the same number of iterations as with the oracle solve, to
+    the same optimum."""
+    nlp = dist.NLP(dist.Instance(10))
+    r_o = ipm.solve_nlp(nlp, OracleKKT(nlp), max_iter=100)
+    nlp_g = dist.NLP(dist.Instance(10))
+    r_g = ipm.solve_nlp(nlp_g, ipm.GpuKKT(nlp_g.n, nlp_g.m, nlp_g.pat.w_row, nlp_g.pat.w_col, nlp_g.pat.j_rowptr,
+                                          nlp_g.pat.j_col), max_iter=100)
+    _check_solution(nlp, r_o)
+    _check_solution(nlp_g, r_g)
+    assert r_g.iterations == r_o.iterations
+    assert abs(r_g.objective - r_o.objective) <= 1e-8 * max(1.0, abs(r_o.objective))
+    assert np.abs(r_g.v - r_o.v).max() <= 1e-6
