@@ -82,6 +82,8 @@ typedef struct {
   const int32_t *perm;         /* optional host [n] caller ordering (new -> old); NULL = built-in ND */
   int32_t device;              /* CUDA device ordinal; -1 = host-only analysis (no device resources) */
   void *stream;                /* cudaStream_t owned by the caller; NULL = legacy default stream */
+  double cg_rtol_corr;         /* CG stop of the refinement passes' corrections (HyKKT), default 1e-6:
+                                  the refinement test ref_tol still decides the final accuracy (R6) */
 } ckkt_options;
 
 typedef struct {

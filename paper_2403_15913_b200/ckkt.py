@@ -37,7 +37,7 @@ class ckkt_options(ctypes.Structure):
     _fields_ = [("strategy", ctypes.c_int32), ("gamma", ctypes.c_double), ("cg_rtol", ctypes.c_double),
                 ("cg_maxit", ctypes.c_int32), ("ref_tol", ctypes.c_double), ("ref_maxit", ctypes.c_int32),
                 ("batch", ctypes.c_int32), ("leaf", ctypes.c_int32), ("perm", ctypes.c_void_p),
-                ("device", ctypes.c_int32), ("stream", ctypes.c_void_p)]
+                ("device", ctypes.c_int32), ("stream", ctypes.c_void_p), ("cg_rtol_corr", ctypes.c_double)]
 
 
 class ckkt_info(ctypes.Structure):

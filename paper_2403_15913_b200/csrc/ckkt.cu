@@ -325,8 +325,8 @@ __global__ void k_cg_update_xr(int me, const double* __restrict__ alpha, const d
 
 // rr_new from partials; convergence test ||r|| <= rtol ||b||; beta
 __global__ void k_cg_beta(int B, const double* __restrict__ part, double* __restrict__ rr, const double* __restrict__ bnorm2,
-                          double rtol, double* __restrict__ beta, int* __restrict__ done, int* __restrict__ iters,
-                          int* __restrict__ active) {
+                          const double* __restrict__ rtolp, double* __restrict__ beta, int* __restrict__ done,
+                          int* __restrict__ iters, int* __restrict__ active) {
   const int b = blockIdx.x;  // one block per instance
   if (done[b]) {
     if (threadIdx.x == 0) beta[b] = 0.0;
@@ -337,7 +337,7 @@ __global__ void k_cg_beta(int B, const double* __restrict__ part, double* __rest
     iters[b] += 1;
     beta[b] = t / rr[b];
     rr[b] = t;
-    if (sqrt(t) <= rtol * sqrt(bnorm2[b])) done[b] = 1;
+    if (sqrt(t) <= rtolp[0] * sqrt(bnorm2[b])) done[b] = 1;
     else atomicAdd(active, 1);
   }
 }
@@ -807,6 +807,8 @@ struct ckkt_ctx {
   double *rho1 = nullptr, *rho2 = nullptr, *rho3 = nullptr, *rho4 = nullptr;
   double *rho1b = nullptr, *rho2b = nullptr, *rho3b = nullptr, *rho4b = nullptr;
   double *part = nullptr, *omega = nullptr, *resinf = nullptr, *wnorm_dev = nullptr;
+  double* cg_rtol_dev = nullptr;  // [3]: first-pass / correction-pass / current CG tolerance
+  double cg_rtol_corr = 1e-10;
   double *cg_rr = nullptr, *cg_bn = nullptr, *cg_alpha = nullptr, *cg_beta = nullptr;
   int *cg_done = nullptr, *cg_iters = nullptr, *active = nullptr, *accflag = nullptr, *skipflag = nullptr;
   int* h_pinned_int = nullptr;
@@ -1211,6 +1213,13 @@ ckkt_status setup_device(ckkt_ctx* c) {
   DALLOC(c->omega, 2 * B);
   DALLOC(c->resinf, 2 * B);
   DALLOC(c->wnorm_dev, B);
+  DALLOC(c->cg_rtol_dev, 3);
+  {
+    c->cg_rtol_corr = c->opt.cg_rtol_corr;
+    if (const char* e = getenv("CKKT_CG_RTOL_CORR")) c->cg_rtol_corr = atof(e);  // A/B experiments only
+    const double h[3] = {c->opt.cg_rtol, c->cg_rtol_corr, c->opt.cg_rtol};
+    CK(cudaMemcpy(c->cg_rtol_dev, h, sizeof(h), cudaMemcpyHostToDevice));
+  }
   DALLOC(c->cg_rr, B);
   DALLOC(c->cg_bn, B);
   DALLOC(c->cg_alpha, B);
@@ -1252,6 +1261,7 @@ void ckkt_default_options(ckkt_options* o) {
   o->strategy = CKKT_HYKKT;
   o->gamma = 1e7;
   o->cg_rtol = 1e-10;
+  o->cg_rtol_corr = 1e-6;
   o->cg_maxit = 200;
   o->ref_tol = 1e-14;
   o->ref_maxit = 10;
@@ -1681,7 +1691,7 @@ void cg_iteration(ckkt_ctx* c) {
                                     c->rec_VN);
   c->launches++;
   dot(c, me, c->cg_r, c->cg_r, c->cg_done);
-  k_cg_beta<<<B, TPB, 0, st>>>(B, c->part, c->cg_rr, c->cg_bn, c->opt.cg_rtol, c->cg_beta, c->cg_done,
+  k_cg_beta<<<B, TPB, 0, st>>>(B, c->part, c->cg_rr, c->cg_bn, c->cg_rtol_dev + 2, c->cg_beta, c->cg_done,
                                      c->cg_iters, c->active);
   k_cg_update_p<<<gme, TPB, 0, st>>>(me, c->cg_beta, c->cg_r, c->cg_p, c->cg_done);
   c->launches += 7;
@@ -1741,6 +1751,10 @@ ckkt_status solve_pass(ckkt_ctx* c, const double* r1, int r1_internal, const dou
                                   skip);
     const bool init_cg = c->rec_on && !first_pass;
     if (c->rec_on) CK(cudaMemsetAsync(c->rec_enable, first_pass ? 1 : 0, sizeof(int), st));
+    // CG stopping tolerance of this pass (slot 2, read by the captured k_cg_beta): slot 0 first pass
+    // (cg_rtol), slot 1 the correction passes (cg_rtol_corr, reading R6)
+    CK(cudaMemcpyAsync(c->cg_rtol_dev + 2, c->cg_rtol_dev + (first_pass ? 0 : 1), sizeof(double),
+                       cudaMemcpyDeviceToDevice, st));
     if (!init_cg) {  // CG: x = 0, r = p = b
       k_zero<<<gme, TPB, 0, st>>>(me, c->cg_x);
       cudaMemcpyAsync(c->cg_r, c->bvec, sizeof(double) * (size_t)B * me, cudaMemcpyDeviceToDevice, st);
@@ -1756,7 +1770,7 @@ ckkt_status solve_pass(ckkt_ctx* c, const double* r1, int r1_internal, const dou
                                        c->cg_p);
       k_dot_partial<<<dim3(DOT_BLOCKS, c->B), TPB, 0, st>>>(me, c->bvec, c->bvec, c->part_b, skip);
       dot(c, me, c->cg_r, c->cg_r, skip);
-      k_cg_init_scalars2<<<B, TPB, 0, st>>>(B, c->part, c->part_b, c->opt.cg_rtol, c->cg_rr, c->cg_bn,
+      k_cg_init_scalars2<<<B, TPB, 0, st>>>(B, c->part, c->part_b, c->cg_rtol_corr, c->cg_rr, c->cg_bn,
                                                   c->cg_done, c->cg_iters, skip);
       k_rec_start_z<<<gn, TPB, 0, st>>>(n, B, c->rec_VN, c->rec_coef, c->rec_n, c->cg_z);
       c->launches += 7;

@@ -35,7 +35,7 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(ckkt.ckkt_pattern) == 4 * 3 + 4 + 8 + 8 * 6
     assert ctypes.sizeof(ckkt.ckkt_info) == 4 * 4 + 8 * 3
     o = ckkt.default_options()
-    assert o.strategy == ckkt.CKKT_HYKKT and o.gamma == 1e7 and o.cg_rtol == 1e-10 and o.cg_maxit == 200
+    assert o.strategy == ckkt.CKKT_HYKKT and o.gamma == 1e7 and o.cg_rtol == 1e-10 and o.cg_maxit == 200 and o.cg_rtol_corr == 1e-6
     assert o.batch == 1 and o.ref_maxit == 10
 
 

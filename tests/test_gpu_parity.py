@@ -120,3 +120,18 @@ def test_gamma_sweep_stress():
     case.sigma_x[:] = np.exp(rng.uniform(np.log(1e-8), np.log(1e8), case.sigma_x.shape))
     for gamma in (1e4, 1e5, 1e6, 1e7, 1e8):
         _check(case, 1, gamma=gamma)
+
+
+@pytest.mark.gpu
+def test_correction_cg_tolerance_does_not_change_the_step():
+    """Reading R6: the refinement passes' CG tolerance (cg_rtol_corr) only changes the work, not the
+    result: at 1e-10 and at the default 1e-6 the refined steps meet the same bars and agree."""
+    case = distillation_case(50, 1, iterates=[3, 11, 16])
+    g_tight = run_gpu(case, 1, cg_rtol_corr=1e-10)
+    g_loose = run_gpu(case, 1)
+    for b in range(case.B):
+        for g in (g_tight, g_loose):
+            assert g["info"][b]["rel_res"] <= RES_TOL
+        assert g_loose["info"][b]["k_cg"] == g_tight["info"][b]["k_cg"]      # first pass unchanged
+        ref = g_tight["dx"][b]
+        assert np.linalg.norm(g_loose["dx"][b] - ref) <= STEP_TOL * np.linalg.norm(ref)
