@@ -73,7 +73,8 @@ class GpuKKT:
         dx = T.empty(self.n, dtype=T.float64, device=self.dev)
         dy = T.empty(self.m, dtype=T.float64, device=self.dev)
         rc, info = self.ctx.solve(self._t(r1), None, self._t(r3), None, dx, None, dy, None)
-        return dx.cpu().numpy(), dy.cpu().numpy(), info[0]
+        # CG / refinement non-convergence still returns the best iterate (include/ckkt.h); reported per step
+        return dx.cpu().numpy(), dy.cpu().numpy(), dict(info[0], rc=int(rc))
 
     def fraction_to_boundary(self, s, ds, tau):
         a = self.ckkt.fraction_to_boundary(self._t(s), self._t(ds), tau)
@@ -83,7 +84,7 @@ class GpuKKT:
 def solve_nlp(problem, kkt, mu0=0.1, tol=1e-6, max_iter=200, alpha_min_frac=0.05, verbose=False) -> IPMResult:
     """Filter line-search IPM (see the module docstring).  `problem` provides n, m, bidx (indices of
     the bounded variables), lo, hi, x0, lam0, f(v), grad_f(v), c(v), jac(v) (J values in the
-    pattern's CSR order), jac_t(v, jv, y) (J^T y), jac_mul(jv, d) (J d) and hess(v, lam) (W values
+    pattern's CSR order), jac_t(v, jv, y) (J^T y) and hess(v, lam) (W values
     of f + lam^T c).  `kkt` provides refactor / solve / fraction_to_boundary (GpuKKT)."""
     P = problem
     b, lo, hi = P.bidx, P.lo, P.hi
@@ -177,7 +178,7 @@ def solve_nlp(problem, kkt, mu0=0.1, tol=1e-6, max_iter=200, alpha_min_frac=0.05
         z_lo = np.clip(z_lo, mu / (KAPPA_SIGMA * sl), KAPPA_SIGMA * mu / sl)
         z_hi = np.clip(z_hi, mu / (KAPPA_SIGMA * su), KAPPA_SIGMA * mu / su)
         hist.append(dict(mu=mu, theta=theta, phi=phi, alpha=alpha, alpha_z=a_z, delta_x=delta, trials=trials,
-                         k_cg=int(info.get("k_cg", 0)) if isinstance(info, dict) else 0, ls=ls))
+                         k_cg=int(info.get("k_cg", 0)), solve_rc=int(info.get("rc", 0)), ls=ls))
         if verbose:
             print(f"it {it:3d} mu {mu:.2e} theta {theta:.2e} phi {phi:.6e} alpha {alpha:.3e} delta {delta:.1e} "
                   f"ls {ls}")
