@@ -113,3 +113,18 @@ def test_pattern_errors():
 def test_device_calls_refuse_host_only_context():
     ctx = _host_ctx(3, 0, 0, np.array([0, 1, 2]), np.array([0, 1, 2]), None, None, None, None)
     assert ckkt.lib().ckkt_refactor(ctx.h, None, None, None, None, None, None, None, None) == ckkt.CKKT_INVALID_ARG
+    assert ckkt.lib().ckkt_refactor_inertia(ctx.h, None, None, None, None, None, None, None, None, None,
+                                            None) == ckkt.CKKT_INVALID_ARG
+
+
+def test_fraction_to_boundary_argument_checks():
+    """Argument validation happens before any device work (no GPU needed): tau outside (0, 1),
+    negative sizes, missing pointers -> CKKT_INVALID_ARG; an empty batch is a no-op."""
+    L = ckkt.lib()
+    dummy = ctypes.c_void_p(8)
+    assert L.ckkt_fraction_to_boundary(1, 4, dummy, dummy, 1.0, dummy, None) == ckkt.CKKT_INVALID_ARG
+    assert L.ckkt_fraction_to_boundary(1, 4, dummy, dummy, 0.0, dummy, None) == ckkt.CKKT_INVALID_ARG
+    assert L.ckkt_fraction_to_boundary(1, -1, dummy, dummy, 0.99, dummy, None) == ckkt.CKKT_INVALID_ARG
+    assert L.ckkt_fraction_to_boundary(1, 4, None, dummy, 0.99, dummy, None) == ckkt.CKKT_INVALID_ARG
+    assert L.ckkt_fraction_to_boundary(1, 4, dummy, dummy, 0.99, None, None) == ckkt.CKKT_INVALID_ARG
+    assert L.ckkt_fraction_to_boundary(0, 4, None, None, 0.99, None, None) == ckkt.CKKT_OK
