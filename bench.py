@@ -8,7 +8,9 @@ Contract (driver): python bench.py [--gpus N --steps K --warmup W] [--impl refer
     per GPU; with N GPUs each rank solves its own instance (different initial state) = weak scaling;
   * value = max-over-ranks device time / (steps x ranks)  [ms per IPM iteration, lower is better];
   * e2e = same metric through ckkt_iterate_host (H2D of the step's values + rhs, D2H of the step);
-  * --impl reference = the CPU oracle (oracle/), timed on a bounded sample on rank 0.
+  * --impl reference = the CPU oracle (oracle/) as it stands, single-threaded, at the same workload and
+    iterates on rank 0 (min(warmup, 1) untimed + min(steps, 3) timed iterations, median);
+  * --gpus N without WORLD_SIZE in the environment re-executes itself under torchrun (N ranks).
 """
 from __future__ import annotations
 
@@ -97,6 +99,29 @@ def dist_init():
     return world, rank, local
 
 
+def trajectory_rhs(n, m, instance, T):
+    """The seeded right-hand sides of one instance's trajectory: r1 [T, n], then r3 (or r2) [T, m], then
+    r4 [T, m], drawn in that order from the generator 3000 + instance (one stream shared by both arms)."""
+    import numpy as np
+    rng = np.random.default_rng(3000 + instance)
+    r1 = np.stack([rng.standard_normal(n) for _ in range(T)])
+    ra = np.stack([rng.standard_normal(m) for _ in range(T)])
+    rb = np.stack([rng.standard_normal(m) for _ in range(T)])
+    return r1, ra, rb
+
+
+def trajectory_positions(inst, ks, per_mu=3):
+    """Iterates at trajectory positions ks (Instance.trajectory()[k] without building the others)."""
+    from inputs import distillation as dist
+    mus = dist.mu_schedule()
+    return {k: inst.iterate(k, mus[k // per_mu]) for k in ks}
+
+
+def trajectory_length(per_mu=3):
+    from inputs import distillation as dist
+    return per_mu * len(dist.mu_schedule())
+
+
 def build_inputs(N, instances, dev):
     """Values of the 18-iterate trajectories of the given instances, stacked [T, B, len] on `dev`."""
     import numpy as np
@@ -107,14 +132,69 @@ def build_inputs(N, instances, dev):
     pat = insts[0].model.pat
     n, m = pat.n, pat.m
     T = len(trajs[0])
-    rngs = [np.random.default_rng(3000 + i) for i in instances]
+    assert T == trajectory_length()
     st = lambda f: torch.as_tensor(np.stack([np.stack([getattr(tr[k], f) for tr in trajs]) for k in range(T)]),
                                    device=dev)
-    rhs = lambda cols: torch.as_tensor(np.stack([np.stack([r.standard_normal(cols) for r in rngs]) for _ in range(T)]),
-                                       device=dev)
+    rh = [trajectory_rhs(n, m, i, T) for i in instances]
+    rhs = lambda j: torch.as_tensor(np.stack([r[j] for r in rh], axis=1), device=dev)  # [T, B, len]
     return {"pat": pat, "n": n, "m": m, "B": len(instances),
             "w": st("w_val"), "j": st("j_val"), "sig": st("sigma_x"), "dl": st("d_lifted"),
-            "r1": rhs(n), "ra": rhs(m), "rb": rhs(m)}
+            "r1": rhs(0), "ra": rhs(1), "rb": rhs(2)}
+
+
+def bench_config(args, world, n, m):
+    """The workload description shared by both arms (same_config)."""
+    N, batch, desc = CONFIGS[args.config]
+    large = N * 67 * 47 * 8 * max(batch, 1) > 126e6  # L factor ~47 doubles per variable (ND, leaf 1072)
+    return {"workload": desc, "N": N, "n": n, "m_e": m, "strategy": "HyKKT gamma=1e7",
+            "instances": batch if batch > 1 else world, "units": "one IPM iteration of one KKT system",
+            "leaf": args.leaf,
+            "l2": ("inputs larger than L2 (factor > 126 MB L2 per GPU); no flush" if large else
+                   "factor L2-resident (< 126 MB); no flush, repeated solves hit L2"),
+            "parallelism": (f"batch sharded over {world} GPU(s), no collective" if batch > 1
+                            else f"replicas x{world} (one instance per GPU, no collective)")}
+
+
+def host_info():
+    import platform
+    model = platform.processor()
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
+def oracle_iterations(N, instance, ks, leaf, warmup=1):
+    """The oracle as it stands (oracle/kkt.py + oracle/csrc), single-threaded (BLAS pools limited to one
+    thread), one HyKKT IPM iteration = refactor + solve per trajectory position in ks, after `warmup`
+    untimed iterations on the first position.  Returns per-iteration seconds and the last Info."""
+    import numpy as np
+    from threadpoolctl import threadpool_limits
+    from inputs import distillation as dist
+    from oracle import kkt as OK
+    inst = dist.Instance(N, instance)
+    its = trajectory_positions(inst, sorted(set(ks)))
+    pat = inst.model.pat
+    T = trajectory_length()
+    r1, ra, _ = trajectory_rhs(pat.n, pat.m, instance, T)
+    e32 = np.zeros(1, np.int32)
+    times, info = [], None
+    with threadpool_limits(limits=1):
+        t = time.perf_counter()
+        o = OK.SparseKKT(pat.n, pat.m, 0, pat.w_row, pat.w_col, pat.j_rowptr, pat.j_col, e32, e32[:0], leaf=leaf)
+        setup_s = time.perf_counter() - t
+        for j, k in enumerate([ks[0]] * warmup + list(ks)):
+            it = its[k]
+            t = time.perf_counter()
+            o.refactor(it.w_val, it.j_val, np.zeros(0), it.sigma_x, np.zeros(0), 0.0)
+            d, info = o.solve(r1[k], np.zeros(0), ra[k], np.zeros(0))
+            if j >= warmup:
+                times.append(time.perf_counter() - t)
+    return times, info, setup_s
 
 
 def run_ckkt(args, world, rank, local):
@@ -237,39 +317,53 @@ def run_ckkt(args, world, rank, local):
             torch.distributed.destroy_process_group()
         return
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
-        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
-    # roofline of the dominant kernel phase: algorithmic bytes per launch
-    #   forward / backward sweep: read every panel once + read/write x   = 8 (l_storage + 2 n)
-    #   factorization:            read K, write L                        = 8 (nnz_k + l_storage)
-    #   condensation:             read W, J, Sigma, maps; write K
-    algo = {"forward": 8.0 * B * (sizes["l_storage"] + 2 * n), "backward": 8.0 * B * (sizes["l_storage"] + 2 * n),
-            "factor": 8.0 * B * (sizes["nnz_k"] + sizes["l_storage"]),
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 7700.0}
+    peak_src = ("measured (MEASURED_PEAKS.json hbm_gbs)" if "when" in peaks
+                else "fallback (B200_PROFILING.md nominal HBM3e)")
+    # algorithmic bytes per launch, from the EXACT factor (nnz_l, no amalgamation padding):
+    #   forward / backward sweep: read every L entry once + read and write x   = 8 (nnz_l + 2 n)
+    #   factorization:            read K, write L                              = 8 (nnz_k + nnz_l)
+    #   condensation:             read W, J, Sigma; write K (maps excluded)    = 8 (nnz_w + nnz_j + n + nnz_k)
+    nnz_l = sizes["nnz_l"]
+    algo = {"forward": 8.0 * B * (nnz_l + 2 * n), "backward": 8.0 * B * (nnz_l + 2 * n),
+            "factor": 8.0 * B * (sizes["nnz_k"] + nnz_l),
             "condense": 8.0 * B * (len(pat.w_row) + len(pat.j_col) + n + sizes["nnz_k"])}
-    dom = max((k for k in phases if k in algo), key=lambda k: phases[k][0])
-    dom_ms, dom_n = phases[dom]
-    avg = dom_ms / max(dom_n, 1)
-    achieved = algo[dom] / (avg * 1e-3) / 1e9
-    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "when" in peaks else "fallback"
-    roof = {"bound": "hbm", "kernel": {"forward": "k_fwd_tiny + k_fwd_persist + k_fwd_top (one forward sweep)",
-                                       "backward": "k_bwd_top + k_bwd_persist + k_bwd_tiny (one backward sweep)",
-                                       "factor": "k_factor_persist", "condense": "k_condense"}[dom],
-            "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
-            "traffic": None, "peak_source": peak_src, "algorithmic_bytes_per_launch": algo[dom],
-            "avg_launch_ms": avg,
-            "phase_pass": "CUDA events per launch group, separate timed pass of min(steps, 3) steps of the same workload",
-            "phases_ms_per_step": {k: v[0] / args.steps for k, v in phases.items()},
-            "launches_per_step": {k: v[1] / args.steps for k, v in phases.items()}}
+    kname = {"forward": "k_fwd_tiny + k_fwd_persist + k_fwd_top (one forward sweep)",
+             "backward": "k_bwd_top + k_bwd_persist + k_bwd_tiny (one backward sweep)",
+             "factor": "k_factor_tiny + k_factor_persist (one numeric factorization)",
+             "condense": "k_condense"}
     tr_path = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tr_path):  # DRAM bytes per launch of this kernel from the committed ncu capture
-        roof["traffic"] = json.load(open(tr_path)).get(roof["kernel"])
+    traffic = json.load(open(tr_path)) if os.path.exists(tr_path) else {}
+
+    def roof_entry(ph):
+        ms_tot, cnt = phases[ph]
+        avg = ms_tot / max(cnt, 1)
+        ach = algo[ph] / (avg * 1e-3) / 1e9
+        return {"bound": "hbm", "kernel": kname[ph], "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": ach / peaks["hbm_gbs"], "traffic": traffic.get(kname[ph]), "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": algo[ph], "avg_launch_ms": avg,
+                "share_of_step": ms_tot / max(sum(v[0] for v in phases.values()), 1e-30)}
+
+    dom = max((k for k in phases if k in algo), key=lambda k: phases[k][0])
+    roof = roof_entry(dom)
+    roof["phase_pass"] = ("CUDA events on the library stream per launch group, separate pass of min(steps, 3) "
+                          "steps of the same workload (host-driven CG loop)")
+    roof["phases_ms_per_step"] = {k: v[0] / args.steps for k, v in phases.items()}
+    roof["launches_per_step"] = {k: v[1] / args.steps for k, v in phases.items()}
+    roof["per_phase"] = {ph: {k: v for k, v in roof_entry(ph).items() if k in ("achieved", "frac", "avg_launch_ms",
+                                                                          "traffic", "share_of_step")}
+                         for ph in algo}
+    # the factorization against the FP64 pipe: algorithmic flops sum_j colcount_j^2 (exact pattern)
     fac_ms = phases["factor"][0] / max(phases["factor"][1], 1)
-    fp64 = {"kernel": "k_factor_persist", "flops": B * sizes["flops_factor"], "ms": fac_ms,
-            "achieved_tflops": B * sizes["flops_factor"] / (fac_ms * 1e-3) / 1e12, "peak_tflops": 37.1,
-            "peak_source": "measured DFMA/DMMA microbenchmark, profiles/fp64_peak_r01.txt"}
-    fp64["frac"] = fp64["achieved_tflops"] / fp64["peak_tflops"]
+    fp64 = {"bound": "fp64", "kernel": kname["factor"], "flops_per_launch": B * sizes["flops_factor"],
+            "ms": fac_ms, "achieved": B * sizes["flops_factor"] / (fac_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+            "peak": 37.1, "peak_source": "measured FP64 DFMA/DMMA microbenchmark on this B200 pool "
+                                         "(profiles/fp64_peak_r01.txt; DMMA m8n8k4 on sm_100a = DFMA rate)"}
+    fp64["frac"] = fp64["achieved"] / fp64["peak"]
+    fp64["hbm"] = roof["per_phase"]["factor"]
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        cpu = cpu_baseline(data, args)
+        cpu = cpu_baseline(args, N, (args.warmup % T))
     info_summary = {"k_cg_mean": float(np.mean([i["k_cg"] for i in infos])),
                     "rel_res_unrefined_max": float(max(i["rel_res_unrefined"] for i in infos)),
                     "n_ref_mean": float(np.mean([i["n_ref"] for i in infos])),
@@ -285,11 +379,8 @@ def run_ckkt(args, world, rank, local):
         "scaling": "strong" if batch > 1 else "weak",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic distillation-column IPM iterates (inputs/distillation.py), random N(0,1) rhs",
-        "config": {"workload": desc, "N": N, "n": n, "m_e": m, "strategy": "HyKKT gamma=1e7",
-                   "instances_per_gpu": B, "units": "one IPM iteration of one KKT system",
-                   "leaf": args.leaf, "l2": "inputs larger than L2 (L factor %.2f GB)" % (sizes["l_storage"] * 8 / 1e9),
-                   "parallelism": f"replicas x{world}"},
+        "data": "synthetic distillation-column IPM iterates (inputs/distillation.py), seeded N(0,1) rhs",
+        "config": bench_config(args, world, n, m),
         "phases_ms": {"refactor": (phases["condense"][0] + phases["factor"][0]) / args.steps,
                       "sweeps": (phases["forward"][0] + phases["backward"][0]) / args.steps,
                       "vector": phases["vector"][0] / args.steps,
@@ -311,72 +402,65 @@ def run_ckkt(args, world, rank, local):
         torch.distributed.destroy_process_group()
 
 
-def cpu_baseline(data, args, N_sample=10000):
-    """The oracle as it stands, single-threaded, one HyKKT IPM iteration (refactor + solve) on a
-    bounded sample: the same model at N_sample stages, scaled to N by the stage count (work per stage
-    is constant for the nested-dissection ordering)."""
-    import numpy as np
-    from inputs import distillation as dist
-    from oracle import kkt as OK
-    N = CONFIGS[args.config][0]
-    Ns = min(N, N_sample)
-    inst = dist.Instance(Ns, 0)
-    it = inst.iterate(9, 1.5e-4)
-    pat = inst.model.pat
-    e32 = np.zeros(1, np.int32)
-    o = OK.SparseKKT(pat.n, pat.m, 0, pat.w_row, pat.w_col, pat.j_rowptr, pat.j_col, e32, e32[:0], leaf=args.leaf)
-    rng = np.random.default_rng(1)
-    t = time.perf_counter()
-    o.refactor(it.w_val, it.j_val, np.zeros(0), it.sigma_x, np.zeros(0), 0.0)
-    d, info = o.solve(rng.standard_normal(pat.n), np.zeros(0), rng.standard_normal(pat.m), np.zeros(0))
-    el = time.perf_counter() - t
-    return {"value": el * 1e3 * (N / Ns), "unit": "ms/IPM-iter", "cores": 1, "kind": "oracle",
-            "sample": f"one HyKKT iteration (refactor+solve, k_cg={info.k_cg}, n_ref={info.n_ref}) at N={Ns}, "
-                      f"scaled x{N / Ns:g} to N={N}; measured {el:.1f} s"}
+def cpu_baseline(args, N, k0):
+    """The oracle as it stands, single-threaded, at the bench's own workload: one HyKKT IPM iteration
+    (refactor + solve) of instance 0 at trajectory position k0 (the first timed GPU step's iterate and
+    rhs), full size.  The oracle has no caches to warm, so the one iteration is timed directly."""
+    times, info, setup_s = oracle_iterations(N, 0, [k0], args.leaf, warmup=0)
+    return {"value": times[0] * 1e3, "unit": "ms/IPM-iter", "cores": 1, "kind": "oracle",
+            "sample": f"one oracle HyKKT iteration (refactor+solve, k_cg={info.k_cg}, n_ref={info.n_ref}) at the "
+                      f"full workload N={N}, trajectory position {k0}; BLAS pools limited to 1 thread; oracle "
+                      f"setup {setup_s:.0f} s excluded (like the GPU setup)", **host_info()}
 
 
 def run_reference(args, world, rank):
-    """--impl reference: the CPU oracle as it stands, on rank 0 only."""
+    """--impl reference: the CPU oracle as it stands, on rank 0 only, at the same workload and iterates as
+    the GPU arm (instance 0, trajectory positions warmup + k): min(warmup, 1) untimed and min(steps, 3)
+    timed iterations, median."""
     if rank != 0:
         return
     import numpy as np
-    from inputs import distillation as dist
-    from oracle import kkt as OK
     N = CONFIGS[args.config][0]
-    Ns = min(N, 2000)
-    inst = dist.Instance(Ns, 0)
-    traj = inst.trajectory()
-    pat = inst.model.pat
-    e32 = np.zeros(1, np.int32)
-    o = OK.SparseKKT(pat.n, pat.m, 0, pat.w_row, pat.w_col, pat.j_rowptr, pat.j_col, e32, e32[:0], leaf=args.leaf)
-    rng = np.random.default_rng(1)
-
-    def step(k):
-        it = traj[k % len(traj)]
-        o.refactor(it.w_val, it.j_val, np.zeros(0), it.sigma_x, np.zeros(0), 0.0)
-        return o.solve(rng.standard_normal(pat.n), np.zeros(0), rng.standard_normal(pat.m), np.zeros(0))
-
-    for k in range(args.warmup):
-        step(k)
-    t = time.perf_counter()
-    for k in range(args.steps):
-        step(args.warmup + k)
-    el = time.perf_counter() - t
-    v = el * 1e3 / args.steps * (N / Ns)
-    sample = f"oracle HyKKT iterations (refactor+solve) at N={Ns}, scaled x{N / Ns:g} to N={N}"
+    T = trajectory_length()
+    wu, ks = min(args.warmup, 1), [(args.warmup + k) % T for k in range(min(args.steps, 3))]
+    times, info, setup_s = oracle_iterations(N, 0, ks, args.leaf, warmup=wu)
+    v = float(np.median(times)) * 1e3
+    from inputs import distillation as dist
+    n, m = dist.dimensions(N)
+    sample = (f"{len(times)} oracle HyKKT iterations (refactor+solve) at the full workload N={N}, trajectory "
+              f"positions {ks} (the GPU arm's first timed iterates), after {wu} untimed; median; BLAS pools "
+              f"limited to 1 thread; per-iteration s = {[float(f"{t:.3g}") for t in times]}; oracle setup "
+              f"{setup_s:.0f} s excluded")
     print(json.dumps({
         "impl": "reference", "metric": "KKT refactor+solve ms/IPM-iter (FP64)", "value": v, "unit": "ms/IPM-iter",
-        "higher_is_better": False, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": v, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic distillation-column IPM iterates", "config": {"workload": CONFIGS[args.config][2], "N": N},
-        "cpu_baseline": {"value": v, "unit": "ms/IPM-iter", "cores": 1, "kind": "oracle", "sample": sample},
+        "higher_is_better": False, "n_gpus": world, "steps": len(times), "steps_requested": args.steps,
+        "warmup": wu, "ms_per_step": v, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic distillation-column IPM iterates (inputs/distillation.py), seeded N(0,1) rhs",
+        "config": bench_config(args, world, n, m),
+        "cpu_baseline": {"value": v, "unit": "ms/IPM-iter", "cores": 1, "kind": "oracle", "sample": sample,
+                         **host_info()},
         "e2e": {"value": v, "unit": "ms/IPM-iter", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
 
+def _free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N` without a launcher: re-exec under torchrun, one rank per GPU (127.0.0.1
+        # rendezvous); rank 0 prints the single JSON line
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+        os.execv(sys.executable, cmd)
     world, rank, local = dist_init()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args, world, rank)
         return

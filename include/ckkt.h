@@ -49,7 +49,8 @@ typedef enum {
   CKKT_OK = 0,
   CKKT_NOT_PD = 1,               /* Cholesky breakdown: wrong inertia. A result, not a failure. */
   CKKT_CG_NO_CONVERGENCE = 2,    /* CG hit cg_maxit; the last iterate is returned */
-  CKKT_REFINE_NOT_CONVERGED = 3, /* refinement stopped above ref_tol; the best iterate is returned */
+  CKKT_REFINE_NOT_CONVERGED = 3, /* refinement stopped with omega > max(ref_tol, 1e-10): the best iterate is
+                                    returned; omega in (ref_tol, 1e-10] (the north-star bar) is OK */
   CKKT_PATTERN_ERROR = 4,        /* malformed pattern (index out of range, unsorted CSR, ...) */
   CKKT_INVALID_ARG = 5,
   CKKT_CUDA_ERROR = 6,
@@ -73,7 +74,7 @@ typedef struct {
 typedef struct {
   int32_t strategy;            /* CKKT_LIFTED or CKKT_HYKKT */
   double gamma;                /* HyKKT augmentation, default 1e7; ignored by Lifted */
-  double cg_rtol;              /* CG stop ||r_k||_2 <= cg_rtol ||b||_2, default 1e-10 (reading R6) */
+  double cg_rtol;              /* CG stop ||r_k||_2 <= cg_rtol ||b||_2, default 1e-10 (reading R6); finite, > 0 */
   int32_t cg_maxit;            /* default 200 */
   double ref_tol;              /* refinement stop on the componentwise backward error, default 1e-14 (R7) */
   int32_t ref_maxit;           /* default 10; 0 = no refinement */
@@ -83,7 +84,11 @@ typedef struct {
   int32_t device;              /* CUDA device ordinal; -1 = host-only analysis (no device resources) */
   void *stream;                /* cudaStream_t owned by the caller; NULL = legacy default stream */
   double cg_rtol_corr;         /* CG stop of the refinement passes' corrections (HyKKT), default 1e-6:
-                                  the refinement test ref_tol still decides the final accuracy (R6) */
+                                  the refinement test ref_tol still decides the final accuracy (R6).
+                                  0 = the default (a zero-initialised struct); negative / non-finite
+                                  values, like non-positive cg_rtol, ref_tol or (HyKKT) gamma and
+                                  negative caps, make ckkt_setup return CKKT_INVALID_ARG.  (Appended
+                                  to the struct in round 1: callers must use this header's layout.) */
 } ckkt_options;
 
 typedef struct {
@@ -126,13 +131,20 @@ ckkt_status ckkt_get_sizes(const ckkt_ctx *ctx, ckkt_sizes *sizes);
 ckkt_status ckkt_export_symbolic(const ckkt_ctx *ctx, int32_t *perm, int32_t *parent, int32_t *colcount,
                                  int64_t *l_colptr, int32_t *l_rowind);
 
+/* Copy the internal elimination order (host memory): order[k] = original index of the column the
+ * numeric factorization eliminates k-th.  It is perm composed with a postorder of its elimination
+ * tree (same fill, contiguous supernodes; reading R11) and is the order in which min_bad_pivot is
+ * defined (reading R9 of P:347-350): a sequential Cholesky of K_gamma permuted by `order` first
+ * fails at position k* with min_bad_pivot == order[k*].  order: [n].  CKKT_INVALID_ARG on NULL. */
+ckkt_status ckkt_export_elimination_order(const ckkt_ctx *ctx, int32_t *order);
+
 /* Numeric refactorization of K_gamma from the values of one IPM iterate.
  *   w_val [B, w_nnz], g_val [B, nnz(G)], h_val [B, nnz(H)], sigma_x [B, n], d_s [B, m_i] (> 0),
  *   delta_x [B]  -- device FP64 (g_val/h_val/d_s may be NULL when the block is empty;
  *   delta_x may be NULL = 0).
  *   not_pd [B] (device int32, may be NULL): set to 1 where some pivot is <= 0 or not finite;
- *   min_bad_pivot [B] (device int32, may be NULL): smallest failing column in the internal
- *   elimination order, -1 if none (reading R9).
+ *   min_bad_pivot [B] (device int32, may be NULL): ORIGINAL index of the failing column that comes
+ *   first in the internal elimination order (ckkt_export_elimination_order), -1 if none (reading R9).
  * Asynchronous: the flags are valid once the stream reaches this point.
  * Zero-copy: the value arrays are read again by ckkt_solve (condensed rhs, SpMVs with G/H,
  * K_aug residual), so they must stay valid and unmodified until the last ckkt_solve that

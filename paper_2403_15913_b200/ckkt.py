@@ -19,7 +19,8 @@ CKKT_OK, CKKT_NOT_PD, CKKT_CG_NO_CONVERGENCE, CKKT_REFINE_NOT_CONVERGED = 0, 1, 
 CKKT_PATTERN_ERROR, CKKT_INVALID_ARG, CKKT_CUDA_ERROR, CKKT_OUT_OF_MEMORY = 4, 5, 6, 7
 CKKT_LIFTED, CKKT_HYKKT = 0, 1
 
-EXPORTED = ["ckkt_default_options", "ckkt_setup", "ckkt_get_sizes", "ckkt_export_symbolic", "ckkt_refactor",
+EXPORTED = ["ckkt_default_options", "ckkt_setup", "ckkt_get_sizes", "ckkt_export_symbolic",
+            "ckkt_export_elimination_order", "ckkt_refactor",
             "ckkt_refactor_inertia", "ckkt_fraction_to_boundary",
             "ckkt_solve", "ckkt_iterate_host", "ckkt_profile", "ckkt_phase_times", "ckkt_launch_count",
             "ckkt_destroy", "ckkt_status_str"]
@@ -78,6 +79,8 @@ def lib():
         L.ckkt_get_sizes.restype = ctypes.c_int
         L.ckkt_export_symbolic.argtypes = [P, P, P, P, P, P]
         L.ckkt_export_symbolic.restype = ctypes.c_int
+        L.ckkt_export_elimination_order.argtypes = [P, P]
+        L.ckkt_export_elimination_order.restype = ctypes.c_int
         L.ckkt_refactor.argtypes = [P, P, P, P, P, P, P, P, P]
         L.ckkt_refactor.restype = ctypes.c_int
         L.ckkt_refactor_inertia.argtypes = [P] * 11
@@ -226,6 +229,14 @@ class Context:
         if rc:
             raise CKKTError(rc, "ckkt_export_symbolic")
         return perm, parent, cc, Lp, Li
+
+    def export_elimination_order(self):
+        """ckkt_export_elimination_order: order[k] = original index eliminated k-th (min_bad_pivot's order)."""
+        order = np.empty(self.n, np.int32)
+        rc = lib().ckkt_export_elimination_order(self.h, _np_ptr(order))
+        if rc:
+            raise CKKTError(rc, "ckkt_export_elimination_order")
+        return order
 
     def profile(self, enable: bool = True):
         rc = lib().ckkt_profile(self.h, int(enable))

@@ -765,6 +765,7 @@ struct ckkt_ctx {
   const SnMeta* qmeta = nullptr;  // metadata of the bottom queue, queue order
   const SnMeta* tmeta = nullptr;  // metadata of the tiny subtrees' nodes, sub_nodes order
   double *gtv = nullptr, *htv = nullptr;  // G / H values in transposed (column) order, refreshed at refactor
+  double* gv = nullptr;  // G values (row order) copied at refactor: the captured CG graph reads only context memory
   int ntop = 0;
   const SnMeta* topmeta = nullptr;  // metadata of the top queue, top order
   int topbuf = 0;                   // doubles of the top kernels' panel buffer
@@ -853,6 +854,8 @@ ckkt_status dalloc(ckkt_ctx* c, void** p, size_t bytes) {
     ckkt_status st_ = dalloc(c, (void**)&(ptr), (size_t)(count) * sizeof(*(ptr))); \
     if (st_ != CKKT_OK) return st_;                                               \
   } while (0)
+
+bool build_cg_graph(ckkt_ctx* c);
 
 ckkt_status setup_device(ckkt_ctx* c) {
   ckkt::Analysis& A = c->A;
@@ -1178,6 +1181,7 @@ ckkt_status setup_device(ckkt_ctx* c) {
   DALLOC(c->epoch_dev, 2);
   CK(cudaMemset(c->epoch_dev, 0, 2 * sizeof(int)));
   DALLOC(c->gtv, (size_t)B * std::max<int64_t>(c->g_nnz, 1));
+  DALLOC(c->gv, (size_t)B * std::max<int64_t>(c->g_nnz, 1));
   DALLOC(c->htv, (size_t)B * std::max<int64_t>(c->h_nnz, 1));
   DALLOC(c->wsv, (size_t)B * std::max<int64_t>(c->ws_nnz, 1));
   DALLOC(c->sig_i, (size_t)B * n);
@@ -1245,6 +1249,29 @@ ckkt_status setup_device(ckkt_ctx* c) {
   DALLOC(c->skipflag, B);
   CK(cudaMallocHost(&c->h_pinned_int, sizeof(int) * (5 * B + 16)));
   CK(cudaMallocHost(&c->h_pinned_dbl, sizeof(double) * (8 * B + 16)));
+  // device staging of ckkt_iterate_host (values, rhs, step): allocated here, never in a per-iteration call
+  DALLOC(c->st_w, (size_t)B * std::max<int64_t>(c->w_nnz, 1));
+  DALLOC(c->st_g, (size_t)B * std::max<int64_t>(c->g_nnz, 1));
+  DALLOC(c->st_h, (size_t)B * std::max<int64_t>(c->h_nnz, 1));
+  DALLOC(c->st_sig, Bn);
+  DALLOC(c->st_ds, Bmi);
+  DALLOC(c->st_del, B);
+  DALLOC(c->st_r1, Bn);
+  DALLOC(c->st_r2, Bmi);
+  DALLOC(c->st_r3, Bme);
+  DALLOC(c->st_r4, Bmi);
+  DALLOC(c->st_dx, Bn);
+  DALLOC(c->st_ds_o, Bmi);
+  DALLOC(c->st_dy, Bme);
+  DALLOC(c->st_dz, Bmi);
+  DALLOC(c->st_notpd, B);
+  // the CG loop graph is captured here too (it reads only context-owned memory)
+  if (me > 0 && c->stream != nullptr && !sync_debug() && !getenv("CKKT_NO_GRAPH")) {
+    if (!build_cg_graph(c)) {
+      c->graph_failed = true;  // the host-driven loop is used instead
+      cudaGetLastError();
+    }
+  }
   return CKKT_OK;
 }
 
@@ -1310,6 +1337,13 @@ ckkt_status ckkt_setup(const ckkt_pattern* p, const ckkt_options* opt, ckkt_ctx*
   if (opt) o = *opt;
   else ckkt_default_options(&o);
   if (o.batch < 1 || (o.strategy != CKKT_LIFTED && o.strategy != CKKT_HYKKT)) return CKKT_INVALID_ARG;
+  // tolerances: finite and > 0 (a zero cg_rtol_corr, e.g. from a zero-initialised struct, means the
+  // default); caps >= 0; gamma finite and > 0 for HyKKT
+  if (o.cg_rtol_corr == 0.0) o.cg_rtol_corr = 1e-6;
+  auto pos = [](double v) { return std::isfinite(v) && v > 0.0; };
+  if (!pos(o.cg_rtol) || !pos(o.cg_rtol_corr) || !pos(o.ref_tol) || o.cg_maxit < 0 || o.ref_maxit < 0 ||
+      (o.strategy == CKKT_HYKKT && !pos(o.gamma)))
+    return CKKT_INVALID_ARG;
   if (o.strategy == CKKT_LIFTED && p->m_e != 0) return CKKT_INVALID_ARG;
   if (p->n <= 0 || p->m_e < 0 || p->m_i < 0 || p->w_nnz < 0) return CKKT_INVALID_ARG;
   if ((p->w_nnz > 0 && (!p->w_row || !p->w_col)) || (p->m_e > 0 && (!p->g_rowptr || !p->g_col)) ||
@@ -1400,6 +1434,12 @@ ckkt_status ckkt_export_symbolic(const ckkt_ctx* c, int32_t* perm, int32_t* pare
   return CKKT_OK;
 }
 
+ckkt_status ckkt_export_elimination_order(const ckkt_ctx* c, int32_t* order) {
+  if (!c || !order) return CKKT_INVALID_ARG;
+  std::copy(c->A.perm2.begin(), c->A.perm2.end(), order);
+  return CKKT_OK;
+}
+
 int64_t ckkt_launch_count(const ckkt_ctx* c) { return c ? c->launches : 0; }
 
 ckkt_status ckkt_profile(ckkt_ctx* c, int32_t enable) {
@@ -1445,6 +1485,9 @@ ckkt_status ckkt_refactor(ckkt_ctx* c, const double* w_val, const double* g_val,
   if (c->g_nnz) {
     k_gather_t<<<(unsigned)((c->g_nnz * B + TPB - 1) / TPB), TPB, 0, st>>>(c->g_nnz, B, c->gt_e, g_val, c->gtv);
     c->launches++;
+    // the CG graph (captured once) and the residual read the context's copy, never the caller's
+    // buffer, so a refactor with a different g_val pointer cannot leave a stale pointer behind
+    CK(cudaMemcpyAsync(c->gv, g_val, sizeof(double) * (size_t)B * c->g_nnz, cudaMemcpyDeviceToDevice, st));
   }
   if (c->h_nnz) {
     k_gather_t<<<(unsigned)((c->h_nnz * B + TPB - 1) / TPB), TPB, 0, st>>>(c->h_nnz, B, c->ht_e, h_val, c->htv);
@@ -1676,7 +1719,7 @@ void cg_iteration(ckkt_ctx* c) {
   prof_end(c);
   ksolve(c, c->vn, c->cg_done);
   prof_begin(c, 4);
-  k_g_spmv<<<gme, TPB, 0, st>>>(me, n, c->g_rowptr, c->g_col2, c->g_val, c->g_nnz, c->vn, 1.0, nullptr, 0.0, c->cg_q,
+  k_g_spmv<<<gme, TPB, 0, st>>>(me, n, c->g_rowptr, c->g_col2, c->gv, c->g_nnz, c->vn, 1.0, nullptr, 0.0, c->cg_q,
                                 c->cg_done);
   dot(c, me, c->cg_p, c->cg_q, c->cg_done);
   k_cg_alpha<<<B, TPB, 0, st>>>(B, c->part, c->cg_rr, c->cg_alpha, c->cg_done, c->cg_iters, c->rec_enable,
@@ -1747,7 +1790,7 @@ ckkt_status solve_pass(ckkt_ctx* c, const double* r1, int r1_internal, const dou
     prof_end(c);
     ksolve(c, c->tn, skip);
     prof_begin(c, 4);
-    k_g_spmv<<<gme, TPB, 0, st>>>(me, n, c->g_rowptr, c->g_col2, c->g_val, c->g_nnz, c->tn, -1.0, r3, 1.0, c->bvec,
+    k_g_spmv<<<gme, TPB, 0, st>>>(me, n, c->g_rowptr, c->g_col2, c->gv, c->g_nnz, c->tn, -1.0, r3, 1.0, c->bvec,
                                   skip);
     const bool init_cg = c->rec_on && !first_pass;
     if (c->rec_on) CK(cudaMemsetAsync(c->rec_enable, first_pass ? 1 : 0, sizeof(int), st));
@@ -1776,12 +1819,8 @@ ckkt_status solve_pass(ckkt_ctx* c, const double* r1, int r1_internal, const dou
       c->launches += 7;
     }
     prof_end(c);
-    const bool use_graph = !c->profiling && !c->graph_failed && !sync_debug() && !getenv("CKKT_NO_GRAPH");
-    if (use_graph && !c->cg_exec && !build_cg_graph(c)) {
-      c->graph_failed = true;  // fall back to the host-driven loop
-      cudaGetLastError();
-    }
-    if (use_graph && c->cg_exec) {
+    const bool use_graph = !c->profiling && c->cg_exec != nullptr;
+    if (use_graph) {
       CK(cudaMemsetAsync(c->active, 0, sizeof(int), st));
       CK(cudaMemsetAsync(c->cg_loop, 0, sizeof(int), st));
       CK(cudaGraphLaunch(c->cg_exec, st));
@@ -1846,7 +1885,7 @@ void residual(ckkt_ctx* c, const double* r1, const double* r2, const double* r3,
   a.gt_ptr = c->gt_ptr; a.gt_e = c->gt_e; a.gt_r = c->gt_r;
   a.ht_ptr = c->ht_ptr; a.ht_e = c->ht_e; a.ht_r = c->ht_r;
   a.g_rowptr = c->g_rowptr; a.g_col2 = c->g_col2; a.h_rowptr = c->h_rowptr; a.h_col2 = c->h_col2;
-  a.w_val = c->w_val; a.g_val = c->g_val; a.h_val = c->h_val; a.sigma = c->sigma; a.d_s = c->d_s; a.delta = c->delta;
+  a.w_val = c->w_val; a.g_val = c->gv; a.h_val = c->h_val; a.sigma = c->sigma; a.d_s = c->d_s; a.delta = c->delta;
   a.gtv = c->gtv; a.htv = c->htv;
   a.w_nnz = c->w_nnz; a.g_nnz = c->g_nnz; a.h_nnz = c->h_nnz;
   a.r1 = r1; a.r2 = r2; a.r3 = r3; a.r4 = r4;
@@ -2001,24 +2040,6 @@ extern "C" ckkt_status ckkt_iterate_host(ckkt_ctx* c, const double* w_val, const
   CK(cudaSetDevice(c->opt.device));
   const int B = c->B;
   const size_t Bn = (size_t)B * c->n, Bme = (size_t)B * c->me, Bmi = (size_t)B * c->mi;
-  if (!c->st_w) {
-    ckkt_status s;
-    if ((s = dalloc(c, (void**)&c->st_w, sizeof(double) * B * std::max<int64_t>(c->w_nnz, 1))) != CKKT_OK) return s;
-    if ((s = dalloc(c, (void**)&c->st_g, sizeof(double) * B * std::max<int64_t>(c->g_nnz, 1))) != CKKT_OK) return s;
-    if ((s = dalloc(c, (void**)&c->st_h, sizeof(double) * B * std::max<int64_t>(c->h_nnz, 1))) != CKKT_OK) return s;
-    if ((s = dalloc(c, (void**)&c->st_sig, sizeof(double) * Bn)) != CKKT_OK) return s;
-    if ((s = dalloc(c, (void**)&c->st_ds, sizeof(double) * std::max<size_t>(Bmi, 1))) != CKKT_OK) return s;
-    if ((s = dalloc(c, (void**)&c->st_del, sizeof(double) * B)) != CKKT_OK) return s;
-    if ((s = dalloc(c, (void**)&c->st_r1, sizeof(double) * Bn)) != CKKT_OK) return s;
-    if ((s = dalloc(c, (void**)&c->st_r2, sizeof(double) * std::max<size_t>(Bmi, 1))) != CKKT_OK) return s;
-    if ((s = dalloc(c, (void**)&c->st_r3, sizeof(double) * std::max<size_t>(Bme, 1))) != CKKT_OK) return s;
-    if ((s = dalloc(c, (void**)&c->st_r4, sizeof(double) * std::max<size_t>(Bmi, 1))) != CKKT_OK) return s;
-    if ((s = dalloc(c, (void**)&c->st_dx, sizeof(double) * Bn)) != CKKT_OK) return s;
-    if ((s = dalloc(c, (void**)&c->st_ds_o, sizeof(double) * std::max<size_t>(Bmi, 1))) != CKKT_OK) return s;
-    if ((s = dalloc(c, (void**)&c->st_dy, sizeof(double) * std::max<size_t>(Bme, 1))) != CKKT_OK) return s;
-    if ((s = dalloc(c, (void**)&c->st_dz, sizeof(double) * std::max<size_t>(Bmi, 1))) != CKKT_OK) return s;
-    if ((s = dalloc(c, (void**)&c->st_notpd, sizeof(int) * B)) != CKKT_OK) return s;
-  }
   cudaStream_t st = c->stream;
   auto h2d = [&](double* dst, const double* src, size_t cnt) -> cudaError_t {
     if (!src || cnt == 0) return cudaSuccess;

@@ -102,22 +102,24 @@ __device__ __forceinline__ int ld_relaxed(const int* p) {
 #ifndef CKKT_POLL_MAX_NS
 #define CKKT_POLL_MAX_NS 64
 #endif
-// Poll with relaxed loads.  Everything a consumer reads from another CTA after the wait (children's
-// update matrices / vectors, the solution entries of ancestors) is read with ld.global.cg, i.e. from
-// L2, the point of coherence, and those loads are issued only after the poll has returned the
-// producer's epoch (control dependency); the producer publishes with st.release after its data
-// writes.  So no acquire fence (MEMBAR + L1 invalidation, ~1 us on the critical path) is needed.
-// -DCKKT_ACQUIRE_FENCE restores the formal acquire.
+// Poll a producer's done flag until it holds `epoch`.  The poll is an ld.acquire.gpu (SASS:
+// LDG.STRONG.GPU + CCTL.IVALL, no MEMBAR): the load that observes the producer's st.release
+// synchronizes-with it (PTX memory model), so every later read of the producer's data — children's
+// update matrices / vectors, ancestors' solution entries, also read with ld.global.cg from L2 — sees
+// the producer's writes.  The successful poll is the acquire itself: no extra round trip on the
+// critical path.  -DCKKT_RELAXED_POLL (timing experiments only) polls with ld.relaxed and relies on
+// the control dependency, which the PTX model does not guarantee.
 __device__ __forceinline__ void wait_epoch(const int* p, int epoch) {
   if (g_debug_nowait) return;
   int ns = 32;
+#ifdef CKKT_RELAXED_POLL
   while (ld_relaxed(p) != epoch) {
+#else
+  while (ld_acquire(p) != epoch) {
+#endif
     __nanosleep(ns);
     ns = ns < CKKT_POLL_MAX_NS ? 2 * ns : CKKT_POLL_MAX_NS;
   }
-#ifdef CKKT_ACQUIRE_FENCE
-  asm volatile("fence.acq_rel.gpu;" ::: "memory");
-#endif
 }
 
 // release-side fence: makes this thread's prior writes visible at gpu scope before the flag store
@@ -204,6 +206,37 @@ __device__ __forceinline__ void extend_add(const double* __restrict__ Uc, int mc
   }
 }
 
+// U = -L21 L21^T (mu x mu, lower, column-major) from the panel in shared memory (ld ldp, L21 at row
+// offset w), on 8x8 DMMA tiles (mma.sync.m8n8k4.f64); warps take tiles round robin.  Rows >= mu and
+// columns >= w read as zero (guards), so the arithmetic is the same for padded and unpadded panels.
+__device__ __forceinline__ void front_update_dmma(const double* Ps, int ldp, int w, int mu, int lane, int warp,
+                                                  int nwarp, double* U) {
+  const int nb = (mu + 7) >> 3;
+  const int ntile = nb * (nb + 1) / 2;
+  const int g = lane >> 2, t4 = lane & 3;
+  for (int tI = warp; tI < ntile; tI += nwarp) {
+    int I = (int)((sqrt(8.0 * tI + 1.0) - 1.0) * 0.5);
+    while ((I + 1) * (I + 2) / 2 <= tI) ++I;
+    while (I * (I + 1) / 2 > tI) --I;
+    const int J = tI - I * (I + 1) / 2;
+    double c0 = 0.0, c1 = 0.0;
+    const int ia = I * 8 + g, ib = J * 8 + g;
+    const double* ra = Ps + w + ia;
+    const double* rb = Ps + w + ib;
+    for (int k = 0; k < w; k += 4) {
+      const int kk = k + t4;
+      const double a = (ia < mu && kk < w) ? ra[kk * ldp] : 0.0;
+      const double b = (ib < mu && kk < w) ? rb[kk * ldp] : 0.0;
+      dmma_8x8x4(c0, c1, a, b);
+    }
+    const int row = I * 8 + g, col = J * 8 + 2 * t4;
+    if (row < mu) {
+      if (col < mu) U[row + (int64_t)col * mu] = -c0;
+      if (col + 1 < mu) U[row + (int64_t)(col + 1) * mu] = -c1;
+    }
+  }
+}
+
 // small supernode, one warp, panel in shared memory (ld = m)
 __device__ void factor_small(const SymDev& S, int s, int b, int tid, double* Ps, double* dsh, double* L, int64_t Lsize,
                              double* Ub, int64_t Usize, const double* __restrict__ Kb, int* notpd, int* minpiv) {
@@ -225,12 +258,10 @@ __device__ void factor_small(const SymDev& S, int s, int b, int tid, double* Ps,
   }
   dfront::dense_blocked<false>(Ps, ldp, w, m, tid, nt, dsh, notpd + b, minpiv + b, f);  // [Z; L21]
   for (int i = tid; i < m * w; i += nt) P[i] = Ps[i];
-  for (int j = 0; j < mu; ++j)  // U_s = -L21 L21^T (lower)
-    for (int i = j + tid; i < mu; i += nt) {
-      double t = 0.0;
-      for (int k = 0; k < w; ++k) t += Ps[w + i + k * ldp] * Ps[w + j + k * ldp];
-      U[i + (int64_t)j * mu] = -t;
-    }
+  // U_s = -L21 L21^T on 8x8 DMMA tiles of the lower triangle: the same tiles, k order and zero
+  // padding (guards instead of zero-filled pads) as factor_big, so a front's update matrix is
+  // bit-identical whichever path factors it (results independent of the batch size)
+  front_update_dmma(Ps, ldp, w, mu, tid & 31, 0, 1, U);
   __syncwarp();
   for (int ci = S.ch_ptr[s]; ci < S.ch_ptr[s + 1]; ++ci) {
     const int c = S.ch_list[ci];
@@ -270,26 +301,7 @@ __device__ void factor_big(const SymDev& S, int s, int b, double* Ps, double* ds
   if (ph) ph[2] = gtimer();
   dfront::dense_blocked<true>(Ps, ldp, w, m, tid, nt, dsh, notpd + b, minpiv + b, f);  // [Z; L21]
   if (ph) ph[3] = gtimer();
-  {  // U_s = -L21 L21^T: 8x8 DMMA tiles of the lower triangle (Z's upper part is zero, pads are zero)
-    const int nb = (mu + 7) >> 3;
-    const int ntile = nb * (nb + 1) / 2;
-    const int g = lane >> 2, t4 = lane & 3;
-    for (int tI = warp; tI < ntile; tI += nwarp) {
-      int I = (int)((sqrt(8.0 * tI + 1.0) - 1.0) * 0.5);
-      while ((I + 1) * (I + 2) / 2 <= tI) ++I;
-      while (I * (I + 1) / 2 > tI) --I;
-      const int J = tI - I * (I + 1) / 2;
-      double c0 = 0.0, c1 = 0.0;
-      const double* ra = Ps + w + I * 8 + g;
-      const double* rb = Ps + w + J * 8 + g;
-      for (int k = 0; k < wp; k += 4) dmma_8x8x4(c0, c1, ra[(k + t4) * mp], rb[(k + t4) * mp]);
-      const int row = I * 8 + g, col = J * 8 + 2 * t4;
-      if (row < mu) {
-        if (col < mu) U[row + (int64_t)col * mu] = -c0;
-        if (col + 1 < mu) U[row + (int64_t)(col + 1) * mu] = -c1;
-      }
-    }
-  }
+  front_update_dmma(Ps, ldp, w, mu, lane, warp, nwarp, U);  // U_s = -L21 L21^T
   if (ph) ph[4] = gtimer();
   for (int e = tid; e < m * w; e += nt) P[e] = Ps[(e % m) + (e / m) * mp];
   __syncthreads();  // this CTA's U_s tile writes are complete before the children add into it

@@ -34,7 +34,7 @@ KAPPA_EPS, KAPPA_MU, THETA_MU, KAPPA_SIGMA = 10.0, 0.2, 1.5, 1e10
 
 @dataclasses.dataclass
 class IPMResult:
-    status: str                 # "converged" | "max_iter" | "restoration" | "inertia_failure"
+    status: str                 # "converged" | "max_iter" | "restoration" | "inertia_failure" | "linear_solver_failure"
     iterations: int
     v: np.ndarray
     lam: np.ndarray
@@ -135,6 +135,13 @@ def solve_nlp(problem, kkt, mu0=0.1, tol=1e-6, max_iter=200, alpha_min_frac=0.05
         r1[b] += -mu / sl + mu / su
         cv = P.c(v)
         dx, dlam, info = kkt.solve(r1, cv)
+        # a step the linear solver could not deliver (NOT_PD / CG non-convergence, or non-finite values)
+        # must not reach the line search; REFINE_NOT_CONVERGED still returns the best (finite) iterate
+        rc = int(info.get("rc", 0))
+        if rc not in (0, 3) or not (np.all(np.isfinite(dx)) and np.all(np.isfinite(dlam))):
+            status = "linear_solver_failure"
+            hist.append(dict(mu=mu, delta_x=delta, trials=trials, k_cg=int(info.get("k_cg", 0)), solve_rc=rc))
+            break
         dzl = mu / sl - z_lo - (z_lo / sl) * dx[b]
         dzu = mu / su - z_hi + (z_hi / su) * dx[b]
         tau = max(0.99, 1.0 - mu)

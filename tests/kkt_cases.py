@@ -140,6 +140,18 @@ def block_errors(gpu, b, d_oracle):
     return errs
 
 
+def elementwise_errors(gpu, b, d_oracle):
+    """Per block: max_i |d_gpu,i - d_oracle,i| / max_i |d_oracle,i| (every element against the block's
+    scale, so no component can hide inside a 2-norm)."""
+    errs = []
+    for name, ref in zip(("dx", "ds", "dy", "dz"), d_oracle):
+        if len(ref) == 0:
+            continue
+        got = gpu[name][b]
+        errs.append(float(np.max(np.abs(got - ref)) / max(np.max(np.abs(ref)), 1e-300)))
+    return errs
+
+
 def host_kaug_backward_error(case: Case, b: int, d):
     """Componentwise backward error of a step computed on the host from the definition (independent
     of both the GPU path and the oracle): max_i |rho_i| / (|K_aug||d| + |r|)_i."""

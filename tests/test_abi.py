@@ -128,3 +128,38 @@ def test_fraction_to_boundary_argument_checks():
     assert L.ckkt_fraction_to_boundary(1, 4, None, dummy, 0.99, dummy, None) == ckkt.CKKT_INVALID_ARG
     assert L.ckkt_fraction_to_boundary(1, 4, dummy, dummy, 0.99, None, None) == ckkt.CKKT_INVALID_ARG
     assert L.ckkt_fraction_to_boundary(0, 4, None, None, 0.99, None, None) == ckkt.CKKT_OK
+
+
+def test_option_validation():
+    """tolerances must be finite and > 0 (cg_rtol_corr = 0 means the default), caps >= 0."""
+    args = (3, 0, 0, np.array([0, 1, 2]), np.array([0, 1, 2]), None, None, None, None)
+    for bad in (dict(cg_rtol=0.0), dict(cg_rtol=float("nan")), dict(cg_rtol_corr=-1.0),
+                dict(cg_rtol_corr=float("inf")), dict(ref_tol=0.0), dict(cg_maxit=-1), dict(ref_maxit=-2),
+                dict(gamma=0.0)):
+        with pytest.raises(ckkt.CKKTError) as e:
+            _host_ctx(*args, **bad)
+        assert e.value.code == ckkt.CKKT_INVALID_ARG, bad
+    _host_ctx(*args, cg_rtol_corr=0.0)          # zero-initialised field: the default
+    _host_ctx(*args, gamma=0.0, strategy=ckkt.CKKT_LIFTED)  # gamma is ignored by Lifted
+
+
+def test_elimination_order_is_a_postorder_of_perm():
+    """ckkt_export_elimination_order (the order min_bad_pivot refers to, reading R9) is a permutation that
+    is a postorder of the exported ordering's elimination tree: every column comes after its descendants and
+    the L pattern it induces has the same size as the exported one (R11)."""
+    pat = dist.build_pattern(30)
+    ctx = _host_ctx(pat.n, pat.m, 0, pat.w_row, pat.w_col, pat.j_rowptr, pat.j_col, None, None, leaf=64)
+    order = ctx.export_elimination_order()
+    perm, parent, cc, Lp, Li = ctx.export_symbolic()
+    assert sorted(order.tolist()) == list(range(pat.n))
+    pos_in_perm = np.empty(pat.n, np.int64)
+    pos_in_perm[perm] = np.arange(pat.n)
+    pos = np.empty(pat.n, np.int64)
+    pos[order] = np.arange(pat.n)
+    for j in range(pat.n):                     # j indexes perm positions; parent[j] is a perm position
+        p = parent[j]
+        if p >= 0:
+            assert pos[perm[j]] < pos[perm[p]]
+    o = OK.SparseKKT(pat.n, pat.m, 0, pat.w_row, pat.w_col, pat.j_rowptr, pat.j_col, E32, E32[:0], perm=order)
+    assert len(o.Li) == len(Li)
+    assert ckkt.lib().ckkt_export_elimination_order(ctx.h, None) == ckkt.CKKT_INVALID_ARG

@@ -5,8 +5,8 @@ error <= 1e-10, integer arrays bit-exact, NOT_PD flag identical, k_CG within +-1
 import numpy as np
 import pytest
 
-from kkt_cases import (block_errors, distillation_case, host_kaug_backward_error, random_case, run_gpu,
-                             run_oracle)
+from kkt_cases import (Case, block_errors, distillation_case, elementwise_errors, host_kaug_backward_error,
+                        random_case, run_gpu, run_oracle)
 
 pytestmark = pytest.mark.gpu
 
@@ -28,6 +28,7 @@ def _check(case, strategy, gamma=1e7, leaf=64, step_tol=STEP_TOL):
             continue
         errs = block_errors(g, b, d)
         assert max(errs) <= step_tol, (b, errs, g["info"][b], info)
+        assert max(elementwise_errors(g, b, d)) <= step_tol, (b, elementwise_errors(g, b, d))
         gi = g["info"][b]
         assert gi["rel_res"] <= RES_TOL, gi
         assert abs(gi["k_cg"] - info.k_cg) <= 1, (gi, info)
@@ -135,3 +136,111 @@ def test_correction_cg_tolerance_does_not_change_the_step():
         assert g_loose["info"][b]["k_cg"] == g_tight["info"][b]["k_cg"]      # first pass unchanged
         ref = g_tight["dx"][b]
         assert np.linalg.norm(g_loose["dx"][b] - ref) <= STEP_TOL * np.linalg.norm(ref)
+
+
+def _oracle_first_failure(case, b, strategy, order, gamma=1e7):
+    """Position of the first failing pivot of the oracle's column Cholesky run in `order`, or -1."""
+    from oracle import kkt as OK
+    E32 = np.zeros(1, np.int32)
+    o = OK.SparseKKT(case.n, case.m_e, case.m_i, case.w_row, case.w_col,
+                     case.g_rowptr if case.m_e else E32, case.g_col if case.m_e else E32[:0],
+                     case.h_rowptr if case.m_i else E32, case.h_col if case.m_i else E32[:0],
+                     strategy=strategy, gamma=gamma, perm=order)
+    return o.refactor(case.w_val[b], case.g_val[b], case.h_val[b], case.sigma_x[b], case.d_s[b], case.delta_x[b])
+
+
+def _shift_some(case, rng, per_instance=3, shift=1e12):
+    """Make each instance indefinite by a large negative shift of Sigma_x on a few random variables;
+    the first of them in the elimination order is where a sequential Cholesky first fails."""
+    for b in range(case.B):
+        idx = rng.choice(case.n, size=per_instance, replace=False)
+        case.sigma_x[b, idx] -= shift
+
+
+@pytest.mark.parametrize("kind", ["random_lifted", "random_hykkt", "distillation_hykkt", "distillation_lifted"])
+def test_min_bad_pivot_matches_oracle_first_failure(kind):
+    """Reading R9: min_bad_pivot is the original index of the failing column that comes first in
+    the internal elimination order.  The oracle's sequential column Cholesky, run in the exported order,
+    must fail first at exactly that column (every earlier pivot is a pivot of a PD leading block)."""
+    import torch
+    rng = np.random.default_rng(hash(kind) % 2**32)
+    if kind == "random_lifted":
+        case, strategy, gamma, leaf = random_case(60, 0, 20, seeds=[31, 32, 33, 34]), 0, 0.0, 8
+    elif kind == "random_hykkt":
+        case, strategy, gamma, leaf = random_case(60, 15, 0, seeds=[41, 42, 43]), 1, 1e4, 8
+    elif kind == "distillation_hykkt":
+        case, strategy, gamma, leaf = distillation_case(50, 1, iterates=[2, 9, 15]), 1, 1e7, 64
+    else:
+        case, strategy, gamma, leaf = distillation_case(50, 0, iterates=[4, 12]), 0, 0.0, 64
+    _shift_some(case, rng)
+    g = run_gpu(case, strategy, gamma=gamma if gamma else 1e7, leaf=leaf)
+    order = g["ctx"].export_elimination_order()
+    assert sorted(order.tolist()) == list(range(case.n))
+    for b in range(case.B):
+        k = _oracle_first_failure(case, b, strategy, order, gamma=gamma if gamma else 1e7)
+        assert k >= 0 and g["notpd"][b] == 1
+        assert g["minpiv"][b] == order[k], (b, k, g["minpiv"][b], order[k])
+    # a positive definite instance reports -1
+    case2 = distillation_case(50, 1, iterates=[5])
+    g2 = run_gpu(case2, 1, leaf=64)
+    assert g2["notpd"][0] == 0 and g2["minpiv"][0] == -1
+
+
+def test_refactor_with_new_value_buffers_matches_fresh_context():
+    """Zero-copy ABI: a second refactor on the same context with DIFFERENT value buffers (the first ones
+    freed) must give exactly what a fresh context gives on those values: the captured CG graph reads
+    only context-owned copies."""
+    import torch
+    from paper_2403_15913_b200 import ckkt
+    dev = torch.device("cuda:0")
+    case = distillation_case(60, 1, iterates=[3, 14])
+    T = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64), device=dev)
+
+    def solve(ctx, k):
+        vals = [T(case.w_val[k]), T(case.g_val[k]), None, T(case.sigma_x[k]), None, None]
+        ctx.refactor(*vals)
+        dx = torch.empty(case.n, dtype=torch.float64, device=dev)
+        dy = torch.empty(case.m_e, dtype=torch.float64, device=dev)
+        rc, info = ctx.solve(T(case.r1[k]), None, T(case.r3[k]), None, dx, None, dy, None)
+        torch.cuda.synchronize()
+        del vals
+        return dx.cpu().numpy(), dy.cpu().numpy(), info[0]
+
+    mk = lambda: ckkt.Context(case.n, case.m_e, 0, case.w_row, case.w_col, case.g_rowptr, case.g_col, None, None,
+                              strategy=1, device=0, stream=torch.cuda.current_stream().cuda_stream)
+    ctx = mk()
+    solve(ctx, 0)
+    torch.cuda.empty_cache()
+    _ = torch.full((4 * case.g_val.shape[1],), float("nan"), dtype=torch.float64, device=dev)  # reuse freed blocks
+    dx1, dy1, i1 = solve(ctx, 1)
+    dx2, dy2, i2 = solve(mk(), 1)
+    assert i1["k_cg"] == i2["k_cg"] and i1["rel_res_unrefined"] == i2["rel_res_unrefined"], (i1, i2)
+    assert np.array_equal(dx1, dx2) and np.array_equal(dy1, dy2)
+
+
+@pytest.mark.parametrize("strategy", [1, 0])
+def test_k_shard_bit_identity(strategy):
+    """per-instance results do not depend on how a batch is sharded.  8 instances solved as
+    1 context x 8, 2 x 4 and 8 x 1 give bit-identical steps (deterministic kernels, same arithmetic for
+    every batch size)."""
+    cases = [distillation_case(60, strategy, iterates=[k], rhs_seed=3000 + k) for k in (0, 2, 5, 7, 9, 11, 14, 17)]
+    c0 = cases[0]
+
+    def stack(sel):
+        f = {k: getattr(c0, k) for k in ("n", "m_e", "m_i", "w_row", "w_col", "g_rowptr", "g_col", "h_rowptr",
+                                         "h_col")}
+        for name in ("w_val", "g_val", "h_val", "sigma_x", "d_s", "delta_x", "r1", "r2", "r3", "r4"):
+            f[name] = np.concatenate([getattr(cases[i], name) for i in sel], axis=0)
+        return Case(**f)
+
+    results = {}
+    for per in (8, 4, 1):
+        outs = []
+        for s0 in range(0, 8, per):
+            g = run_gpu(stack(range(s0, s0 + per)), strategy, leaf=64)
+            outs.append(np.concatenate([g["dx"], g["ds"], g["dy"], g["dz"]], axis=1))
+            for b in range(per):
+                assert g["info"][b]["status"] == 0, g["info"][b]
+        results[per] = np.concatenate(outs, axis=0)
+    assert np.array_equal(results[8].view(np.int64), results[4].view(np.int64))
+    assert np.array_equal(results[8].view(np.int64), results[1].view(np.int64))
