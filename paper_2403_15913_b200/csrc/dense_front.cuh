@@ -177,6 +177,7 @@ __device__ __forceinline__ void dense_blocked(double* Ps, int ldp, int w, int m,
     constexpr int MAXQ = CTA ? 2 : 12;
     double keep[MAXQ][2];
     // T_ij = sum_k L_ik Z_kj  (B = Z not transposed: b = Z[k][n])
+#pragma unroll
     for (int q = 0; q < MAXQ; ++q) {
       const int tI = warp + q * nwarp;
       keep[q][0] = keep[q][1] = 0.0;
@@ -198,6 +199,7 @@ __device__ __forceinline__ void dense_blocked(double* Ps, int ldp, int w, int m,
       }
     }
     group_sync<CTA>();  // every T of block row bi computed before any L_ij is replaced
+#pragma unroll
     for (int q = 0; q < MAXQ; ++q) {
       const int tI = warp + q * nwarp;
       if (tI < ntile) {
@@ -211,6 +213,7 @@ __device__ __forceinline__ void dense_blocked(double* Ps, int ldp, int w, int m,
     }
     group_sync<CTA>();
     // Z_ij = -Zd_i T_ij  (A = Zd_i lower with zero upper part, B = T not transposed)
+#pragma unroll
     for (int q = 0; q < MAXQ; ++q) {
       const int tI = warp + q * nwarp;
       keep[q][0] = keep[q][1] = 0.0;
@@ -227,6 +230,7 @@ __device__ __forceinline__ void dense_blocked(double* Ps, int ldp, int w, int m,
       }
     }
     group_sync<CTA>();
+#pragma unroll
     for (int q = 0; q < MAXQ; ++q) {
       const int tI = warp + q * nwarp;
       if (tI < ntile) {

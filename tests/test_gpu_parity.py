@@ -104,10 +104,10 @@ def test_not_pd_instance_in_hykkt_batch():
         assert g["info"][b]["rel_res"] <= RES_TOL
 
 
-@pytest.mark.parametrize("n,small_panel", [(22, "512"), (30, "1536")])
-def test_one_warp_dense_fronts_wider_than_16(n, small_panel, monkeypatch):
-    """Dense instances whose single front (16 < w <= 32) runs on the one-warp blocked dense path
-    (two 16-column diagonal blocks, Z assembled by one warp)."""
+@pytest.mark.parametrize("n,small_panel", [(22, "512"), (30, "1536"), (60, "512")])
+def test_dense_fronts_wider_than_16(n, small_panel, monkeypatch):
+    """Dense instances whose single front runs the blocked dense path with several 16-column diagonal
+    blocks: 16 < w <= 32 on the one-warp path, w = 60 on a whole CTA."""
     monkeypatch.setenv("CKKT_SMALL_PANEL", small_panel)
     case = random_case(n, 4, 0, seeds=[21, 22], density=1.0)
     _check(case, 1, gamma=1e4, leaf=n)
@@ -244,3 +244,17 @@ def test_k_shard_bit_identity(strategy):
         results[per] = np.concatenate(outs, axis=0)
     assert np.array_equal(results[8].view(np.int64), results[4].view(np.int64))
     assert np.array_equal(results[8].view(np.int64), results[1].view(np.int64))
+
+
+@pytest.mark.parametrize("strategy", [1, 0])
+def test_front_paths_bit_identical(strategy, monkeypatch):
+    """The factorization's front paths (one-warp fronts and whole-CTA fronts) use the same arithmetic in the
+    same order, so moving every front onto the CTA path (CKKT_SMALL_PANEL=64) or letting more fronts onto
+    the one-warp path must not change a single bit of the step."""
+    case = distillation_case(120, strategy, iterates=[4, 13])
+    ref = run_gpu(case, strategy, leaf=268)
+    for panel in ("64", "1536"):
+        monkeypatch.setenv("CKKT_SMALL_PANEL", panel)
+        g = run_gpu(case, strategy, leaf=268)
+        for name in ("dx", "ds", "dy", "dz"):
+            assert np.array_equal(g[name].view(np.int64), ref[name].view(np.int64)), (panel, name)
