@@ -1069,6 +1069,33 @@ ckkt_status setup_device(ckkt_ctx* c) {
         }
         lp.push_back((int32_t)q.size());
       }
+      {  // panel storage in sweep order: tiny subtrees (subtree by subtree, postorder), then the bottom
+         // queue, then the top set, so every worker's supernodes occupy one contiguous span of L
+        std::vector<int64_t> np(ns + 1, -1);
+        int64_t off = 0;
+        auto place = [&](int s2) {
+          np[s2] = off;
+          off += (int64_t)(A.srowptr[s2 + 1] - A.srowptr[s2]) * (A.sfirst[s2 + 1] - A.sfirst[s2]);
+        };
+        for (int s2 : sn) place(s2);
+        for (int s2 : q) place(s2);
+        for (int s2 : tq) place(s2);
+        if (off != A.pofs[ns]) return CKKT_INVALID_ARG;  // every supernode placed exactly once
+        for (int s2 = 0; s2 < ns; ++s2) {
+          A.pofs[s2] = np[s2];
+          c->meta_h[s2].pofs = np[s2];
+        }
+        CK(cudaMemcpy(const_cast<int64_t*>(c->S.pofs), A.pofs.data(), sizeof(int64_t) * A.pofs.size(),
+                      cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(const_cast<SnMeta*>(c->S.meta), c->meta_h.data(), sizeof(SnMeta) * ns, cudaMemcpyHostToDevice));
+        std::vector<SnMeta> tm(sn.size());
+        for (size_t k = 0; k < sn.size(); ++k) {
+          tm[k] = c->meta_h[sn[k]];
+          tm[k].pad1 = sn[k];
+        }
+        if (!sn.empty())
+          CK(cudaMemcpy(const_cast<SnMeta*>(c->tmeta), tm.data(), sizeof(SnMeta) * sn.size(), cudaMemcpyHostToDevice));
+      }
       c->nq = (int)q.size();
       c->ntop = (int)tq.size();
       c->queue = upload(q, o, by);

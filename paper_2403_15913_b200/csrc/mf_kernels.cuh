@@ -586,6 +586,11 @@ __device__ __forceinline__ void warp_stage_chunk(const SymDev& S, const SweepArg
   constexpr int WPM = sizeof(SnMeta) / 8;
   for (int k = lane; k < n * WPM; k += LW) dst[k] = __ldg(src + k);
   wsync();
+  if (lane == 0 && n > 0) {  // the chunk's panels are one contiguous span of L (sweep-ordered storage)
+    const SnMeta& a = msh[0];
+    const SnMeta& z = msh[n - 1];
+    prefetch_l2(A.L + b * A.Lsize + a.pofs, 8ll * (z.pofs + (int64_t)z.m * z.w - a.pofs));
+  }
   if (lane < n && rows) {
     const SnMeta& M = msh[lane];
     prefetch_l2(S.srows + M.r0 + M.w, 4ll * (M.m - M.w));
@@ -1053,6 +1058,10 @@ __global__ void __launch_bounds__(256)
   double* x = X + (int64_t)b * n;
   double* Vbb = Vb + b * Vsize;
   const int q1 = sub_ptr[sub + 1];
+  if (g == 0) {  // the subtree's panels are one contiguous span of L (sweep-ordered storage)
+    const SnMeta a = tmeta[sub_ptr[sub]], z = tmeta[q1 - 1];
+    prefetch_l2(L + b * Lsize + a.pofs, 8ll * (z.pofs + (int64_t)z.m * z.w - a.pofs));
+  }
   for (int q = sub_ptr[sub]; q < q1; ++q) {
     const SnMeta M = tmeta[q];
     const int f = M.f, w = M.w, m = M.m;
@@ -1108,6 +1117,10 @@ __global__ void __launch_bounds__(256)
   auto red = red_all[threadIdx.x / TG];
   double* x = X + (int64_t)b * n;
   const int q0 = sub_ptr[sub];
+  if (g == 0) {  // contiguous span of the subtree's panels
+    const SnMeta a = tmeta[q0], z = tmeta[sub_ptr[sub + 1] - 1];
+    prefetch_l2(L + b * Lsize + a.pofs, 8ll * (z.pofs + (int64_t)z.m * z.w - a.pofs));
+  }
   for (int q = sub_ptr[sub + 1] - 1; q >= q0; --q) {
     const SnMeta M = tmeta[q];
     const int f = M.f, w = M.w, m = M.m;
