@@ -222,6 +222,16 @@ def run_ckkt(args, world, rank, local):
                        leaf=args.leaf, batch=B, device=local, stream=stream.cuda_stream)
     setup_s = time.time() - t1
     sizes = ctx.get_sizes()
+    # NEXT-2: the analysis exported once and reused by a second context
+    t2 = time.time()
+    blob = ctx.export_analysis()
+    export_s = time.time() - t2
+    t2 = time.time()
+    ckkt.Context(n, m, 0, pat.w_row, pat.w_col, pat.j_rowptr, pat.j_col, None, None, strategy=ckkt.CKKT_HYKKT,
+                 leaf=args.leaf, batch=B, device=local, stream=stream.cuda_stream, analysis=blob).close()
+    setup_blob_s = time.time() - t2
+    blob_bytes = int(blob.size)
+    del blob
     dx = torch.empty((B, n), dtype=torch.float64, device=dev)
     dy = torch.empty((B, m), dtype=torch.float64, device=dev)
     notpd = torch.zeros(B, dtype=torch.int32, device=dev)
@@ -389,6 +399,8 @@ def run_ckkt(args, world, rank, local):
         "lifted": lifted,
         "sizes": sizes,
         "setup_s": setup_s,
+        "setup_from_analysis_s": setup_blob_s,
+        "analysis_blob": {"bytes": blob_bytes, "export_s": export_s, "threads": os.cpu_count()},
         "gen_s": t1 - t0,
         "roofline": roof,
         "factor_fp64": fp64,

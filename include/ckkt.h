@@ -121,6 +121,18 @@ void ckkt_default_options(ckkt_options *opt);
  * Returns CKKT_PATTERN_ERROR / CKKT_INVALID_ARG / CKKT_OUT_OF_MEMORY / CKKT_CUDA_ERROR. */
 ckkt_status ckkt_setup(const ckkt_pattern *pattern, const ckkt_options *opt, ckkt_ctx **out);
 
+/* Serialized analysis (the symbolic analysis depends on the pattern only, "can be done
+ * offline" and reused across processes).  ckkt_export_analysis writes the analysis of ctx to buf
+ * (host memory): with buf == NULL it only stores the required size in *size; otherwise *size is the
+ * capacity of buf on entry and the bytes written on exit (CKKT_INVALID_ARG if too small).  The blob
+ * records a hash of the pattern, the leaf size, whether a caller ordering was used and the amalgamation
+ * parameters.  ckkt_setup_from_analysis = ckkt_setup without the analysis: the blob must come from the
+ * same pattern and settings (else CKKT_INVALID_ARG); the context is identical to a freshly analysed
+ * one (same arrays, bit-exact results).  The blob is not referenced after the call. */
+ckkt_status ckkt_export_analysis(const ckkt_ctx *ctx, void *buf, int64_t *size);
+ckkt_status ckkt_setup_from_analysis(const ckkt_pattern *pattern, const ckkt_options *opt, const void *blob,
+                                     int64_t size, ckkt_ctx **out);
+
 /* Sizes of the analysis (host call, no synchronisation). */
 ckkt_status ckkt_get_sizes(const ckkt_ctx *ctx, ckkt_sizes *sizes);
 

@@ -20,7 +20,7 @@ CKKT_PATTERN_ERROR, CKKT_INVALID_ARG, CKKT_CUDA_ERROR, CKKT_OUT_OF_MEMORY = 4, 5
 CKKT_LIFTED, CKKT_HYKKT = 0, 1
 
 EXPORTED = ["ckkt_default_options", "ckkt_setup", "ckkt_get_sizes", "ckkt_export_symbolic",
-            "ckkt_export_elimination_order", "ckkt_refactor",
+            "ckkt_export_elimination_order", "ckkt_export_analysis", "ckkt_setup_from_analysis", "ckkt_refactor",
             "ckkt_refactor_inertia", "ckkt_fraction_to_boundary",
             "ckkt_solve", "ckkt_iterate_host", "ckkt_profile", "ckkt_phase_times", "ckkt_launch_count",
             "ckkt_destroy", "ckkt_status_str"]
@@ -81,6 +81,11 @@ def lib():
         L.ckkt_export_symbolic.restype = ctypes.c_int
         L.ckkt_export_elimination_order.argtypes = [P, P]
         L.ckkt_export_elimination_order.restype = ctypes.c_int
+        L.ckkt_export_analysis.argtypes = [P, P, ctypes.POINTER(ctypes.c_int64)]
+        L.ckkt_export_analysis.restype = ctypes.c_int
+        L.ckkt_setup_from_analysis.argtypes = [ctypes.POINTER(ckkt_pattern), ctypes.POINTER(ckkt_options), P,
+                                               ctypes.c_int64, ctypes.POINTER(P)]
+        L.ckkt_setup_from_analysis.restype = ctypes.c_int
         L.ckkt_refactor.argtypes = [P, P, P, P, P, P, P, P, P]
         L.ckkt_refactor.restype = ctypes.c_int
         L.ckkt_refactor_inertia.argtypes = [P] * 11
@@ -167,7 +172,9 @@ class Context:
     """Owns one ckkt_ctx.  Method names follow the C ABI (ckkt_<name>)."""
 
     def __init__(self, n, m_e, m_i, w_row, w_col, g_rowptr=None, g_col=None, h_rowptr=None, h_col=None,
-                 perm=None, stream=None, **options):
+                 perm=None, stream=None, analysis=None, **options):
+        """analysis: optional bytes from export_analysis() of the same pattern and settings
+        (ckkt_setup_from_analysis: no symbolic analysis at setup)."""
         L = lib()
         self._keep = []
 
@@ -192,9 +199,14 @@ class Context:
         self.opt = opt
         self.n, self.m_e, self.m_i, self.batch = n, m_e, m_i, opt.batch
         h = ctypes.c_void_p()
-        rc = L.ckkt_setup(ctypes.byref(pat), ctypes.byref(opt), ctypes.byref(h))
+        if analysis is None:
+            rc = L.ckkt_setup(ctypes.byref(pat), ctypes.byref(opt), ctypes.byref(h))
+        else:
+            buf = np.frombuffer(analysis, dtype=np.uint8)  # zero-copy view (bytes or a uint8 array)
+            rc = L.ckkt_setup_from_analysis(ctypes.byref(pat), ctypes.byref(opt), buf.ctypes.data_as(ctypes.c_void_p),
+                                            buf.size, ctypes.byref(h))
         if rc != CKKT_OK:
-            raise CKKTError(rc, "ckkt_setup")
+            raise CKKTError(rc, "ckkt_setup" if analysis is None else "ckkt_setup_from_analysis")
         self.h = h
         self._keep = []
 
@@ -229,6 +241,19 @@ class Context:
         if rc:
             raise CKKTError(rc, "ckkt_export_symbolic")
         return perm, parent, cc, Lp, Li
+
+    def export_analysis(self) -> np.ndarray:
+        """ckkt_export_analysis: the serialized symbolic analysis as a uint8 array (reusable with
+        Context(..., analysis=...); .tofile() / np.fromfile() store it)."""
+        size = ctypes.c_int64(0)
+        rc = lib().ckkt_export_analysis(self.h, None, ctypes.byref(size))
+        if rc:
+            raise CKKTError(rc, "ckkt_export_analysis")
+        buf = np.empty(size.value, dtype=np.uint8)
+        rc = lib().ckkt_export_analysis(self.h, buf.ctypes.data_as(ctypes.c_void_p), ctypes.byref(size))
+        if rc:
+            raise CKKTError(rc, "ckkt_export_analysis")
+        return buf
 
     def export_elimination_order(self):
         """ckkt_export_elimination_order: order[k] = original index eliminated k-th (min_bad_pivot's order)."""

@@ -13,6 +13,10 @@
 #include "analysis.h"
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <functional>
+#include <thread>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -35,38 +39,63 @@ const AmalgamationParams& amalgamation_params() {
   return P;
 }
 
+// host threads of the analysis (CKKT_THREADS, default: the hardware concurrency, at most 64); every
+// parallel step below produces exactly the arrays of the sequential algorithm
+static int analysis_threads() {
+  const int t = [] {
+    if (const char* e = getenv("CKKT_THREADS")) return std::max(1, atoi(e));
+    const unsigned h = std::thread::hardware_concurrency();
+    return (int)std::max(1u, std::min(h, 64u));
+  }();
+  return t;
+}
+
+// run f(i) for i in [0, count) on the analysis threads (dynamic assignment; f must be thread safe)
+static void parallel_for(int64_t count, const std::function<void(int64_t, int)>& f) {
+  const int T = (int)std::min<int64_t>(analysis_threads(), std::max<int64_t>(count, 1));
+  if (T <= 1) {
+    for (int64_t i = 0; i < count; ++i) f(i, 0);
+    return;
+  }
+  std::atomic<int64_t> next(0);
+  std::vector<std::thread> th;
+  for (int t = 0; t < T; ++t)
+    th.emplace_back([&, t] {
+      for (int64_t i; (i = next.fetch_add(1)) < count;) f(i, t);
+    });
+  for (auto& x : th) x.join();
+}
+
 // ----------------------------------------------------------------------------
 // ordering
 // ----------------------------------------------------------------------------
 namespace {
 
-struct NDState {
-  int n;
+// Relaxed atomic accesses to the shared label / visit tags: concurrent splits work on disjoint vertex
+// sets and only READ foreign vertices' labels (every tag is drawn once from one atomic counter, so a
+// foreign tag never equals the reader's), so relaxed atomics suffice.
+inline int32_t ald(const int32_t* p) { return __atomic_load_n(p, __ATOMIC_RELAXED); }
+inline void ast(int32_t* p, int32_t v) { __atomic_store_n(p, v, __ATOMIC_RELAXED); }
+
+struct NDGraph {
   const std::vector<int32_t>& xadj;
   const std::vector<int32_t>& adj;
-  int leaf;
-  std::vector<int32_t> label, visit, loc;
-  int setid = 0, version = 0;
-  std::vector<int32_t> out;
-  bool too_big = false;
-
-  NDState(int n_, const std::vector<int32_t>& x, const std::vector<int32_t>& a, int lf)
-      : n(n_), xadj(x), adj(a), leaf(lf), label(n_, 0), visit(n_, 0), loc(n_, -1) {
-    out.reserve(n_);
-  }
+  int32_t *label, *visit;
+  std::atomic<int32_t>* tags;
+  int tag() const { return tags->fetch_add(1) + 1; }
 
   // BFS level sets of G[label == lab] from r; each level sorted ascending.
-  void bfs(int lab, int r, std::vector<std::vector<int32_t>>& levels) {
+  void bfs(int lab, int r, std::vector<std::vector<int32_t>>& levels) const {
     levels.clear();
-    int ver = ++version;
+    const int ver = tag();
     std::vector<int32_t> cur{r}, nxt;
     visit[r] = ver;
     while (!cur.empty()) {
       nxt.clear();
       for (int v : cur)
         for (int p = xadj[v]; p < xadj[v + 1]; ++p) {
-          int a = adj[p];
-          if (label[a] == lab && visit[a] != ver) {
+          const int a = adj[p];
+          if (ald(label + a) == lab && visit[a] != ver) {
             visit[a] = ver;
             nxt.push_back(a);
           }
@@ -79,106 +108,17 @@ struct NDState {
 
   int deg_in(int lab, int v) const {
     int d = 0;
-    for (int p = xadj[v]; p < xadj[v + 1]; ++p) d += (label[adj[p]] == lab);
+    for (int p = xadj[v]; p < xadj[v + 1]; ++p) d += (ald(label + adj[p]) == lab);
     return d;
   }
 
-  // exact minimum degree on the elimination graph of G[C], bitset rows; ties -> smaller index
-  void md(const std::vector<int32_t>& C) {
-    const int k = (int)C.size();
-    if (k == 0) return;
-    if (k > 32768) { too_big = true; return; }
-    const int words = (k + 63) / 64;
-    std::vector<uint64_t> B((size_t)k * words, 0ull);
-    for (int i = 0; i < k; ++i) loc[C[i]] = i;
-    for (int i = 0; i < k; ++i) {
-      int v = C[i];
-      for (int p = xadj[v]; p < xadj[v + 1]; ++p) {
-        int l = loc[adj[p]];
-        if (l >= 0 && l != i) B[(size_t)i * words + (l >> 6)] |= 1ull << (l & 63);
-      }
-    }
-    for (int i = 0; i < k; ++i) loc[C[i]] = -1;
-    std::vector<int> deg(k);
-    std::vector<char> gone(k, 0);
-    for (int i = 0; i < k; ++i) {
-      int d = 0;
-      for (int w = 0; w < words; ++w) d += __builtin_popcountll(B[(size_t)i * words + w]);
-      deg[i] = d;
-    }
-    std::vector<int> nb;
-    for (int step = 0; step < k; ++step) {
-      int v = -1;
-      for (int i = 0; i < k; ++i)
-        if (!gone[i] && (v < 0 || deg[i] < deg[v])) v = i;
-      out.push_back(C[v]);
-      gone[v] = 1;
-      const uint64_t* rv = &B[(size_t)v * words];
-      nb.clear();
-      for (int w = 0; w < words; ++w) {
-        uint64_t x = rv[w];
-        while (x) {
-          int b = __builtin_ctzll(x);
-          nb.push_back(w * 64 + b);
-          x &= x - 1;
-        }
-      }
-      for (int a : nb) {
-        uint64_t* ra = &B[(size_t)a * words];
-        int d = 0;
-        for (int w = 0; w < words; ++w) {
-          ra[w] |= rv[w];
-        }
-        ra[a >> 6] &= ~(1ull << (a & 63));
-        ra[v >> 6] &= ~(1ull << (v & 63));
-        for (int w = 0; w < words; ++w) d += __builtin_popcountll(ra[w]);
-        deg[a] = d;
-      }
-    }
-  }
-
-  void component(std::vector<int32_t>& C) {
-    if ((int)C.size() <= leaf) { md(C); return; }
-    int lab = ++setid;
-    for (int v : C) label[v] = lab;
-    std::vector<std::vector<int32_t>> lev, lev2;
-    bfs(lab, C[0], lev);
-    for (;;) {
-      const auto& last = lev.back();
-      int x = -1, xd = 0;
-      for (int v : last) {  // ascending; strict improvement keeps the smaller index on ties
-        int d = deg_in(lab, v);
-        if (x < 0 || d < xd) { x = v; xd = d; }
-      }
-      bfs(lab, x, lev2);
-      if (lev2.size() > lev.size()) lev.swap(lev2);
-      else break;
-    }
-    const int h = (int)lev.size() - 1;
-    if (h < 2) { md(C); return; }
-    const int ilo = std::max(1, h / 3), ihi = std::min(h - 1, h - h / 3);
-    int bi = -1;
-    for (int i = ilo; i <= ihi; ++i) {
-      if (bi < 0) { bi = i; continue; }
-      size_t sz = lev[i].size(), bsz = lev[bi].size();
-      int c = std::abs(2 * i - h), bc = std::abs(2 * bi - h);
-      if (sz < bsz || (sz == bsz && c < bc)) bi = i;
-    }
-    std::vector<int32_t> S = lev[bi];  // sorted
-    std::vector<int32_t> rest;
-    rest.reserve(C.size() - S.size());
-    std::set_difference(C.begin(), C.end(), S.begin(), S.end(), std::back_inserter(rest));
-    lev.clear(); lev2.clear();
-    rec(rest);
-    out.insert(out.end(), S.begin(), S.end());
-  }
-
-  void rec(std::vector<int32_t>& V) {
+  // connected components of G[V] (V ascending), each sorted, in order of their smallest vertex
+  void components(const std::vector<int32_t>& V, std::vector<std::vector<int32_t>>& comps) const {
+    comps.clear();
     if (V.empty()) return;
-    int lab = ++setid;
-    for (int v : V) label[v] = lab;
-    int ver = ++version;
-    std::vector<std::vector<int32_t>> comps;
+    const int lab = tag();
+    for (int v : V) ast(label + v, lab);
+    const int ver = tag();
     std::vector<int32_t> stack;
     for (int v : V) {
       if (visit[v] == ver) continue;
@@ -186,21 +126,56 @@ struct NDState {
       stack.assign(1, v);
       visit[v] = ver;
       while (!stack.empty()) {
-        int x = stack.back();
+        const int x = stack.back();
         stack.pop_back();
         comp.push_back(x);
         for (int p = xadj[x]; p < xadj[x + 1]; ++p) {
-          int a = adj[p];
-          if (label[a] == lab && visit[a] != ver) { visit[a] = ver; stack.push_back(a); }
+          const int a = adj[p];
+          if (ald(label + a) == lab && visit[a] != ver) {
+            visit[a] = ver;
+            stack.push_back(a);
+          }
         }
       }
       std::sort(comp.begin(), comp.end());
       comps.push_back(std::move(comp));
     }
-    for (auto& c : comps) {
-      if (too_big) return;
-      component(c);
+  }
+
+  // one nested-dissection step on the connected component C (|C| > leaf): the separator S (sorted) and
+  // the components of C \ S; returns false when C is to be ordered by minimum degree instead (h < 2)
+  bool split(const std::vector<int32_t>& C, std::vector<int32_t>& S, std::vector<std::vector<int32_t>>& comps) const {
+    const int lab = tag();
+    for (int v : C) ast(label + v, lab);
+    std::vector<std::vector<int32_t>> lev, lev2;
+    bfs(lab, C[0], lev);
+    for (;;) {  // pseudo-peripheral vertex (George-Liu)
+      const auto& last = lev.back();
+      int x = -1, xd = 0;
+      for (int v : last) {  // ascending; strict improvement keeps the smaller index on ties
+        const int d = deg_in(lab, v);
+        if (x < 0 || d < xd) { x = v; xd = d; }
+      }
+      bfs(lab, x, lev2);
+      if (lev2.size() > lev.size()) lev.swap(lev2);
+      else break;
     }
+    const int h = (int)lev.size() - 1;
+    if (h < 2) return false;
+    const int ilo = std::max(1, h / 3), ihi = std::min(h - 1, h - h / 3);
+    int bi = -1;
+    for (int i = ilo; i <= ihi; ++i) {
+      if (bi < 0) { bi = i; continue; }
+      const size_t sz = lev[i].size(), bsz = lev[bi].size();
+      const int c = std::abs(2 * i - h), bc = std::abs(2 * bi - h);
+      if (sz < bsz || (sz == bsz && c < bc)) bi = i;
+    }
+    S = lev[bi];
+    std::vector<int32_t> rest;
+    rest.reserve(C.size() - S.size());
+    std::set_difference(C.begin(), C.end(), S.begin(), S.end(), std::back_inserter(rest));
+    components(rest, comps);
+    return true;
   }
 };
 
@@ -277,7 +252,10 @@ void permuted_csc(int n, const std::vector<int64_t>& kpairs, const std::vector<i
     int i = iperm[key / n], j = iperm[key % n];
     ri[nx[std::min(i, j)]++] = std::max(i, j);
   }
-  for (int j = 0; j < n; ++j) std::sort(ri.begin() + cp[j], ri.begin() + cp[j + 1]);
+  parallel_for((n + 4095) / 4096, [&](int64_t c, int) {
+    for (int64_t j = c * 4096; j < std::min<int64_t>(n, (c + 1) * 4096); ++j)
+      std::sort(ri.begin() + cp[j], ri.begin() + cp[j + 1]);
+  });
 }
 
 int64_t find_slot(const std::vector<int64_t>& cp, const std::vector<int32_t>& ri, int i, int j) {
@@ -290,17 +268,159 @@ int64_t find_slot(const std::vector<int64_t>& cp, const std::vector<int32_t>& ri
 
 }  // namespace
 
+// Exact minimum degree on the elimination graph of G[C]: bitset rows, ties -> smaller
+// index.  loc: scratch of n entries, all -1 on entry and on exit.
+static void md_order(const std::vector<int32_t>& C, const std::vector<int32_t>& xadj, const std::vector<int32_t>& adj,
+                     std::vector<int32_t>& loc, std::vector<int32_t>& out) {
+  const int k = (int)C.size();
+  out.clear();
+  if (k == 0) return;
+  const int words = (k + 63) / 64;
+  std::vector<uint64_t> B((size_t)k * words, 0ull);
+  for (int i = 0; i < k; ++i) loc[C[i]] = i;
+  for (int i = 0; i < k; ++i) {
+    int v = C[i];
+    for (int p = xadj[v]; p < xadj[v + 1]; ++p) {
+      int l = loc[adj[p]];
+      if (l >= 0 && l != i) B[(size_t)i * words + (l >> 6)] |= 1ull << (l & 63);
+    }
+  }
+  for (int i = 0; i < k; ++i) loc[C[i]] = -1;
+  std::vector<int> deg(k);
+  std::vector<char> gone(k, 0);
+  for (int i = 0; i < k; ++i) {
+    int d = 0;
+    for (int w = 0; w < words; ++w) d += __builtin_popcountll(B[(size_t)i * words + w]);
+    deg[i] = d;
+  }
+  std::vector<int> nb;
+  out.reserve(k);
+  for (int step = 0; step < k; ++step) {
+    int v = -1;
+    for (int i = 0; i < k; ++i)
+      if (!gone[i] && (v < 0 || deg[i] < deg[v])) v = i;
+    out.push_back(C[v]);
+    gone[v] = 1;
+    const uint64_t* rv = &B[(size_t)v * words];
+    nb.clear();
+    for (int w = 0; w < words; ++w) {
+      uint64_t x = rv[w];
+      while (x) {
+        int b = __builtin_ctzll(x);
+        nb.push_back(w * 64 + b);
+        x &= x - 1;
+      }
+    }
+    for (int a : nb) {
+      uint64_t* ra = &B[(size_t)a * words];
+      int d = 0;
+      for (int w = 0; w < words; ++w) ra[w] |= rv[w];
+      ra[a >> 6] &= ~(1ull << (a & 63));
+      ra[v >> 6] &= ~(1ull << (v & 63));
+      for (int w = 0; w < words; ++w) d += __builtin_popcountll(ra[w]);
+      deg[a] = d;
+    }
+  }
+}
+
 std::vector<int32_t> nd_order(int n, const std::vector<int32_t>& xadj, const std::vector<int32_t>& adj, int leaf) {
-  NDState st(n, xadj, adj, std::max(1, leaf));
-  std::vector<int32_t> V(n);
-  std::iota(V.begin(), V.end(), 0);
-  st.rec(V);
-  if (st.too_big || (int)st.out.size() != n) return {};
-  return st.out;
+  // The ordering of DESIGN.md §5, evaluated breadth first: every nested-dissection level splits all of
+  // its components in parallel (they are disjoint), the leaf blocks' minimum-degree orders are computed
+  // in parallel, and the output is the in-order walk of the dissection tree (the components of C \ S in
+  // order of their smallest vertex, then S) — exactly the sequence of the sequential recursion.
+  leaf = std::max(1, leaf);
+  std::vector<int32_t> label(n, 0), visit(n, 0);
+  std::atomic<int32_t> tags(0);
+  NDGraph G{xadj, adj, label.data(), visit.data(), &tags};
+  struct Node {
+    std::vector<int32_t> C;  // vertex set (leaf: ordered later by minimum degree)
+    std::vector<int32_t> S;  // separator (split nodes)
+    std::vector<int> kids;   // child components in order
+    bool is_leaf = false;
+  };
+  std::vector<Node> nodes(1);  // node 0: the whole graph, split into its components (no separator)
+  {
+    std::vector<int32_t> V(n);
+    std::iota(V.begin(), V.end(), 0);
+    std::vector<std::vector<int32_t>> comps;
+    G.components(V, comps);
+    for (auto& c : comps) {
+      nodes[0].kids.push_back((int)nodes.size());
+      nodes.emplace_back();
+      nodes.back().C = std::move(c);
+    }
+  }
+  std::vector<int> frontier(nodes[0].kids);
+  std::atomic<bool> too_big(false);
+  while (!frontier.empty()) {
+    const int nf = (int)frontier.size();
+    std::vector<std::vector<std::vector<int32_t>>> kids(nf);
+    parallel_for(nf, [&](int64_t i, int) {
+      Node& nd = nodes[frontier[i]];
+      if ((int)nd.C.size() <= leaf || !G.split(nd.C, nd.S, kids[i])) {
+        nd.is_leaf = true;
+        if (nd.C.size() > 32768) too_big = true;
+      }
+    });
+    if (too_big) return {};
+    std::vector<int> next;
+    for (int i = 0; i < nf; ++i) {
+      const int id = frontier[i];
+      if (nodes[id].is_leaf) continue;
+      std::vector<int32_t>().swap(nodes[id].C);
+      for (auto& c : kids[i]) {
+        const int k = (int)nodes.size();
+        nodes.emplace_back();
+        nodes.back().C = std::move(c);
+        nodes[id].kids.push_back(k);
+        next.push_back(k);
+      }
+    }
+    frontier.swap(next);
+  }
+  // leaf blocks: exact minimum degree, in parallel (largest first)
+  std::vector<int> lv;
+  for (int i = 0; i < (int)nodes.size(); ++i)
+    if (nodes[i].is_leaf) lv.push_back(i);
+  std::stable_sort(lv.begin(), lv.end(), [&](int x, int y) { return nodes[x].C.size() > nodes[y].C.size(); });
+  std::vector<std::vector<int32_t>> ord(nodes.size());
+  std::vector<std::vector<int32_t>> loc(analysis_threads());
+  parallel_for((int64_t)lv.size(), [&](int64_t i, int t) {
+    if (loc[t].empty()) loc[t].assign(n, -1);
+    md_order(nodes[lv[i]].C, xadj, adj, loc[t], ord[lv[i]]);
+  });
+  // in-order walk: kids, then the separator
+  std::vector<int32_t> out;
+  out.reserve(n);
+  std::vector<std::pair<int, int>> st{{0, 0}};
+  while (!st.empty()) {
+    auto& [id, k] = st.back();
+    const Node& nd = nodes[id];
+    if (nd.is_leaf) {
+      out.insert(out.end(), ord[id].begin(), ord[id].end());
+      st.pop_back();
+    } else if (k < (int)nd.kids.size()) {
+      const int c = nd.kids[k++];
+      st.push_back({c, 0});
+    } else {
+      out.insert(out.end(), nd.S.begin(), nd.S.end());
+      st.pop_back();
+    }
+  }
+  if ((int)out.size() != n) return {};
+  return out;
 }
 
 std::string analyze(const Pattern& p, int leaf, const int32_t* user_perm, Analysis& A, int& code) {
   code = CKKT_OK;
+  const bool verbose = getenv("CKKT_VERBOSE") != nullptr;
+  auto t_prev = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!verbose) return;
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "ckkt analyze: %-28s %8.3f s\n", what, std::chrono::duration<double>(t - t_prev).count());
+    t_prev = t;
+  };
   const int n = p.n;
   A.pat = p;
   A.n = n;
@@ -324,44 +444,77 @@ std::string analyze(const Pattern& p, int leaf, const int32_t* user_perm, Analys
   if (!check_csr(p.me, p.g_rowptr, p.g_col)) { code = CKKT_PATTERN_ERROR; return "G CSR malformed"; }
   if (!check_csr(p.mi, p.h_rowptr, p.h_col)) { code = CKKT_PATTERN_ERROR; return "H CSR malformed"; }
 
-  // ---- K pattern: sorted unique lower pairs (i >= j), original indices
-  std::vector<int64_t>& kp = A.kpairs;
-  kp.clear();
-  int64_t est = (int64_t)p.w_row.size() + n;
-  auto count_pairs = [&](const std::vector<int32_t>& rp) {
-    for (size_t r = 0; r + 1 < rp.size(); ++r) { int64_t k = rp[r + 1] - rp[r]; est += k * (k - 1) / 2; }
-  };
-  count_pairs(p.g_rowptr);
-  count_pairs(p.h_rowptr);
-  kp.reserve(est);
-  for (int i = 0; i < n; ++i) kp.push_back((int64_t)i * n + i);
-  for (size_t e = 0; e < p.w_row.size(); ++e) kp.push_back((int64_t)p.w_row[e] * n + p.w_col[e]);
-  auto add_pairs = [&](int m, const std::vector<int32_t>& rp, const std::vector<int32_t>& ci) {
-    for (int r = 0; r < m; ++r)
-      for (int a = rp[r]; a < rp[r + 1]; ++a)
-        for (int b = rp[r]; b < a; ++b) kp.push_back((int64_t)ci[a] * n + ci[b]);  // ci[a] > ci[b]
-  };
-  add_pairs(p.me, p.g_rowptr, p.g_col);
-  add_pairs(p.mi, p.h_rowptr, p.h_col);
-  std::sort(kp.begin(), kp.end());
-  kp.erase(std::unique(kp.begin(), kp.end()), kp.end());
-  // adjacency (no self loops), ascending
-  A.xadj.assign(n + 1, 0);
-  for (int64_t key : kp) {
-    int i = key / n, j = key % n;
-    if (i != j) { A.xadj[i + 1]++; A.xadj[j + 1]++; }
-  }
-  for (int i = 0; i < n; ++i) A.xadj[i + 1] += A.xadj[i];
-  A.adj.resize(A.xadj[n]);
+  // ---- K pattern = W ∪ G^T G ∪ H^T H ∪ diag: adjacency lists (ascending, no self loops) built per vertex
+  //      in parallel from the rows containing it; then the sorted unique lower pairs (i >= j) row by row
   {
-    std::vector<int32_t> nx(A.xadj.begin(), A.xadj.end() - 1);
-    for (int64_t key : kp) {
-      int i = key / n, j = key % n;
-      if (i != j) { A.adj[nx[i]++] = j; A.adj[nx[j]++] = i; }
+    auto transpose_rows = [&](int m, const std::vector<int32_t>& rp, const std::vector<int32_t>& ci,
+                              std::vector<int64_t>& tp, std::vector<int32_t>& tr) {
+      tp.assign(n + 1, 0);
+      for (int64_t q = 0; q < rp[m]; ++q) tp[ci[q] + 1]++;
+      for (int i = 0; i < n; ++i) tp[i + 1] += tp[i];
+      tr.resize(tp[n]);
+      std::vector<int64_t> nx(tp.begin(), tp.end() - 1);
+      for (int r = 0; r < m; ++r)
+        for (int q = rp[r]; q < rp[r + 1]; ++q) tr[nx[ci[q]]++] = r;
+    };
+    std::vector<int64_t> gtp, htp, wtp;
+    std::vector<int32_t> gtr, htr, wnb;
+    transpose_rows(p.me, p.g_rowptr, p.g_col, gtp, gtr);
+    transpose_rows(p.mi, p.h_rowptr, p.h_col, htp, htr);
+    {  // W neighbours (both triangles)
+      wtp.assign(n + 1, 0);
+      for (size_t e = 0; e < p.w_row.size(); ++e)
+        if (p.w_row[e] != p.w_col[e]) { wtp[p.w_row[e] + 1]++; wtp[p.w_col[e] + 1]++; }
+      for (int i = 0; i < n; ++i) wtp[i + 1] += wtp[i];
+      wnb.resize(wtp[n]);
+      std::vector<int64_t> nx(wtp.begin(), wtp.end() - 1);
+      for (size_t e = 0; e < p.w_row.size(); ++e)
+        if (p.w_row[e] != p.w_col[e]) { wnb[nx[p.w_row[e]]++] = p.w_col[e]; wnb[nx[p.w_col[e]]++] = p.w_row[e]; }
     }
-    for (int i = 0; i < n; ++i) std::sort(A.adj.begin() + A.xadj[i], A.adj.begin() + A.xadj[i + 1]);
+    std::vector<std::vector<int32_t>> nbs(n);
+    const int64_t CH = 4096;
+    parallel_for((n + CH - 1) / CH, [&](int64_t c, int) {
+      std::vector<int32_t> buf;
+      for (int64_t i = c * CH; i < std::min<int64_t>(n, (c + 1) * CH); ++i) {
+        buf.clear();
+        for (int64_t q = wtp[i]; q < wtp[i + 1]; ++q) buf.push_back(wnb[q]);
+        for (int64_t q = gtp[i]; q < gtp[i + 1]; ++q) {
+          const int r = gtr[q];
+          for (int t = p.g_rowptr[r]; t < p.g_rowptr[r + 1]; ++t) buf.push_back(p.g_col[t]);
+        }
+        for (int64_t q = htp[i]; q < htp[i + 1]; ++q) {
+          const int r = htr[q];
+          for (int t = p.h_rowptr[r]; t < p.h_rowptr[r + 1]; ++t) buf.push_back(p.h_col[t]);
+        }
+        std::sort(buf.begin(), buf.end());
+        buf.erase(std::unique(buf.begin(), buf.end()), buf.end());
+        buf.erase(std::remove(buf.begin(), buf.end(), (int32_t)i), buf.end());
+        nbs[i] = buf;
+      }
+    });
+    A.xadj.assign(n + 1, 0);
+    for (int i = 0; i < n; ++i) A.xadj[i + 1] = A.xadj[i] + (int32_t)nbs[i].size();
+    A.adj.resize(A.xadj[n]);
+    std::vector<int64_t> kofs(n + 1, 0);  // lower pairs of row i: neighbours j < i, then (i, i)
+    for (int i = 0; i < n; ++i)
+      kofs[i + 1] = kofs[i] + 1 + (std::lower_bound(nbs[i].begin(), nbs[i].end(), (int32_t)i) - nbs[i].begin());
+    std::vector<int64_t>& kp = A.kpairs;
+    kp.resize(kofs[n]);
+    parallel_for((n + CH - 1) / CH, [&](int64_t c, int) {
+      for (int64_t i = c * CH; i < std::min<int64_t>(n, (c + 1) * CH); ++i) {
+        std::copy(nbs[i].begin(), nbs[i].end(), A.adj.begin() + A.xadj[i]);
+        int64_t o = kofs[i];
+        for (int32_t j : nbs[i]) {
+          if (j > i) break;
+          kp[o++] = i * (int64_t)n + j;
+        }
+        kp[o] = i * (int64_t)n + i;
+        std::vector<int32_t>().swap(nbs[i]);
+      }
+    });
   }
-
+  std::vector<int64_t>& kp = A.kpairs;
+  lap("K pattern + adjacency");
   // ---- ordering
   if (user_perm) {
     A.perm.assign(user_perm, user_perm + n);
@@ -376,6 +529,7 @@ std::string analyze(const Pattern& p, int leaf, const int32_t* user_perm, Analys
   }
   std::vector<int32_t> iperm(n);
   for (int k = 0; k < n; ++k) iperm[A.perm[k]] = k;
+  lap("ordering");
 
   // ---- exported symbolic: etree and column counts for perm
   {
@@ -384,12 +538,11 @@ std::string analyze(const Pattern& p, int leaf, const int32_t* user_perm, Analys
     permuted_csc(n, kp, iperm, cp, ri);
     row_lists(n, cp, ri, rp, rc);
     etree_liu(n, rp, rc, A.parent);
-    row_subtrees(n, rp, rc, A.parent, A.colcount, nullptr, nullptr);
-    A.nnz_l = 0;
-    A.flops = 0.0;
-    for (int j = 0; j < n; ++j) { A.nnz_l += A.colcount[j]; A.flops += (double)A.colcount[j] * A.colcount[j]; }
+    // the column counts follow from the internal symbolic below (a postorder relabels the etree and
+    // the column counts without changing them)
   }
 
+  lap("exported symbolic");
   // ---- postorder of the etree (children ascending) -> internal ordering perm2
   std::vector<int32_t> post;
   post.reserve(n);
@@ -427,9 +580,19 @@ std::string analyze(const Pattern& p, int leaf, const int32_t* user_perm, Analys
     std::vector<int32_t> rc;
     permuted_csc(n, kp, A.iperm2, A.kp, A.ki);
     row_lists(n, A.kp, A.ki, rp, rc);
-    etree_liu(n, rp, rc, A.parent2);
+    // etree of the postordered matrix = the etree of perm relabeled by the postorder
+    std::vector<int32_t> ipost(n);
+    for (int k = 0; k < n; ++k) ipost[post[k]] = k;
+    A.parent2.resize(n);
+    for (int k = 0; k < n; ++k) A.parent2[k] = A.parent[post[k]] < 0 ? -1 : ipost[A.parent[post[k]]];
     row_subtrees(n, rp, rc, A.parent2, A.colcount2, &Lp2, &Li2);
+    A.colcount.resize(n);
+    for (int k = 0; k < n; ++k) A.colcount[post[k]] = A.colcount2[k];
+    A.nnz_l = 0;
+    A.flops = 0.0;
+    for (int j = 0; j < n; ++j) { A.nnz_l += A.colcount[j]; A.flops += (double)A.colcount[j] * A.colcount[j]; }
   }
+  lap("postorder + internal symbolic");
   // ---- fundamental supernodes (fs*), then relaxed amalgamation into the internal supernodes
   std::vector<int32_t> fsfirst, fsof(n), fsparent;
   {
@@ -551,6 +714,7 @@ std::string analyze(const Pattern& p, int leaf, const int32_t* user_perm, Analys
     std::vector<int32_t> nx(A.level_ptr.begin(), A.level_ptr.end() - 1);
     for (int s = 0; s < ns; ++s) A.level_list[nx[A.slevel[s]]++] = s;
   }
+  lap("supernodes + levels");
   // ---- multifrontal maps: children lists (ascending), relative positions of each supernode's
   //      off-diagonal rows inside its parent's rows, update-matrix and update-vector offsets
   {
@@ -592,20 +756,23 @@ std::string analyze(const Pattern& p, int leaf, const int32_t* user_perm, Analys
       }
     }
   }
+  lap("multifrontal maps");
   // ---- condensation maps
   const int64_t nnzk = A.kp[n];
   A.kmap.resize(nnzk);
-  for (int j = 0; j < n; ++j) {
-    int s = A.snode_of[j];
-    int f = A.sfirst[s];
-    const int32_t* sr = &A.srows[A.srowptr[s]];
-    const int ms = (int)(A.srowptr[s + 1] - A.srowptr[s]);
-    int t = 0;
-    for (int64_t k = A.kp[j]; k < A.kp[j + 1]; ++k) {
-      while (t < ms && sr[t] < A.ki[k]) ++t;
-      A.kmap[k] = (int32_t)((int64_t)(j - f) * ms + t);  // relative to the panel start pofs[s]
+  parallel_for((n + 4095) / 4096, [&](int64_t c, int) {
+    for (int j = (int)(c * 4096); j < std::min<int64_t>(n, (c + 1) * 4096); ++j) {
+      int s = A.snode_of[j];
+      int f = A.sfirst[s];
+      const int32_t* sr = &A.srows[A.srowptr[s]];
+      const int ms = (int)(A.srowptr[s + 1] - A.srowptr[s]);
+      int t = 0;
+      for (int64_t k = A.kp[j]; k < A.kp[j + 1]; ++k) {
+        while (t < ms && sr[t] < A.ki[k]) ++t;
+        A.kmap[k] = (int32_t)((int64_t)(j - f) * ms + t);  // relative to the panel start pofs[s]
+      }
     }
-  }
+  });
   // W terms
   {
     std::vector<int64_t> slot_of(p.w_row.size());
@@ -627,34 +794,66 @@ std::string analyze(const Pattern& p, int leaf, const int32_t* user_perm, Analys
   for (int j = 0; j < n; ++j) A.dslot[j] = (int32_t)A.kp[j];  // diagonal = first row of column j
   // J^T D J product terms
   {
-    std::vector<int64_t> slots;
-    std::vector<int32_t> ta, tb, tr;
-    auto gen = [&](int m, const std::vector<int32_t>& rp, const std::vector<int32_t>& ci, int roff) {
-      for (int r = 0; r < m; ++r)
-        for (int a = rp[r]; a < rp[r + 1]; ++a)
-          for (int b = rp[r]; b <= a; ++b) {
-            int i = A.iperm2[ci[a]], j = A.iperm2[ci[b]];
-            slots.push_back(find_slot(A.kp, A.ki, std::max(i, j), std::min(i, j)));
-            ta.push_back(a);
-            tb.push_back(b);
-            tr.push_back(r + roff);
-          }
-    };
-    gen(p.me, p.g_rowptr, p.g_col, 0);
-    gen(p.mi, p.h_rowptr, p.h_col, p.me);
-    A.jt_ptr.assign(nnzk + 1, 0);
-    for (int64_t s : slots) A.jt_ptr[s + 1]++;
-    for (int64_t k = 0; k < nnzk; ++k) A.jt_ptr[k + 1] += A.jt_ptr[k];
-    A.jt_a.resize(slots.size());
-    A.jt_b.resize(slots.size());
-    A.jt_r.resize(slots.size());
-    std::vector<int64_t> nx(A.jt_ptr.begin(), A.jt_ptr.end() - 1);
-    for (size_t t = 0; t < slots.size(); ++t) {
-      int64_t o = nx[slots[t]]++;
-      A.jt_a[o] = ta[t];
-      A.jt_b[o] = tb[t];
-      A.jt_r[o] = tr[t];
+    // product terms of slot (i, j): one per row r of G (weight gamma) or H (weight d_r) containing both
+    // variables, ordered by r (G rows first) — entries a >= b of row r.  Built per K column in parallel
+    // by intersecting the two variables' row lists (count pass, then fill pass).
+    std::vector<int64_t> vp(n + 1, 0);  // row lists of every original variable: (row id, entry index)
+    std::vector<int32_t> vr, ve;
+    {
+      for (int64_t q = 0; q < p.g_rowptr[p.me]; ++q) vp[p.g_col[q] + 1]++;
+      for (int64_t q = 0; q < p.h_rowptr[p.mi]; ++q) vp[p.h_col[q] + 1]++;
+      for (int i = 0; i < n; ++i) vp[i + 1] += vp[i];
+      vr.resize(vp[n]);
+      ve.resize(vp[n]);
+      std::vector<int64_t> nx(vp.begin(), vp.end() - 1);
+      for (int r = 0; r < p.me; ++r)
+        for (int q = p.g_rowptr[r]; q < p.g_rowptr[r + 1]; ++q) { const int64_t o = nx[p.g_col[q]]++; vr[o] = r; ve[o] = q; }
+      for (int r = 0; r < p.mi; ++r)
+        for (int q = p.h_rowptr[r]; q < p.h_rowptr[r + 1]; ++q) {
+          const int64_t o = nx[p.h_col[q]]++;
+          vr[o] = p.me + r;
+          ve[o] = q;
+        }
     }
+    auto each_term = [&](int64_t k, int j, auto&& fn) {  // terms of slot k (internal row ki[k], column j)
+      const int u = A.perm2[A.ki[k]], v = A.perm2[j];     // original variables
+      int64_t x = vp[u], y = vp[v];
+      while (x < vp[u + 1] && y < vp[v + 1]) {
+        if (vr[x] < vr[y]) ++x;
+        else if (vr[x] > vr[y]) ++y;
+        else {
+          const int ea = std::max(ve[x], ve[y]), eb = std::min(ve[x], ve[y]);
+          fn(ea, eb, vr[x]);
+          ++x;
+          ++y;
+        }
+      }
+    };
+    A.jt_ptr.assign(nnzk + 1, 0);
+    parallel_for((n + 4095) / 4096, [&](int64_t c, int) {
+      for (int j = (int)(c * 4096); j < std::min<int64_t>(n, (c + 1) * 4096); ++j)
+        for (int64_t k = A.kp[j]; k < A.kp[j + 1]; ++k) {
+          int64_t cnt = 0;
+          each_term(k, j, [&](int, int, int) { ++cnt; });
+          A.jt_ptr[k + 1] = cnt;
+        }
+    });
+    for (int64_t k = 0; k < nnzk; ++k) A.jt_ptr[k + 1] += A.jt_ptr[k];
+    A.jt_a.resize(A.jt_ptr[nnzk]);
+    A.jt_b.resize(A.jt_ptr[nnzk]);
+    A.jt_r.resize(A.jt_ptr[nnzk]);
+    parallel_for((n + 4095) / 4096, [&](int64_t c, int) {
+      for (int j = (int)(c * 4096); j < std::min<int64_t>(n, (c + 1) * 4096); ++j)
+        for (int64_t k = A.kp[j]; k < A.kp[j + 1]; ++k) {
+          int64_t o = A.jt_ptr[k];
+          each_term(k, j, [&](int ea, int eb, int r) {
+            A.jt_a[o] = ea;
+            A.jt_b[o] = eb;
+            A.jt_r[o] = r;
+            ++o;
+          });
+        }
+    });
   }
   // transposed J by internal column, G and H columns in internal order
   auto transpose = [&](int m, const std::vector<int32_t>& rp, const std::vector<int32_t>& ci, std::vector<int32_t>& tp,
@@ -675,6 +874,133 @@ std::string analyze(const Pattern& p, int leaf, const int32_t* user_perm, Analys
   };
   transpose(p.me, p.g_rowptr, p.g_col, A.gt_ptr, A.gt_e, A.gt_r, A.g_col2);
   transpose(p.mi, p.h_rowptr, p.h_col, A.ht_ptr, A.ht_e, A.ht_r, A.h_col2);
+  lap("condensation maps");
+  return "";
+}
+
+// ---------------------------------------------------------------------------- serialized analysis
+namespace {
+constexpr char kMagic[8] = {'C', 'K', 'K', 'T', 'A', 'N', '0', '1'};
+constexpr uint32_t kVersion = 2;  // bump when the Analysis layout or its algorithms change
+
+template <class F>
+void for_each_array(Analysis& A, F&& f) {  // every array of the analysis, in blob order
+  f(A.kpairs); f(A.perm); f(A.parent); f(A.colcount); f(A.perm2); f(A.iperm2); f(A.kp); f(A.ki);
+  f(A.parent2); f(A.colcount2); f(A.sfirst); f(A.snode_of); f(A.sparent); f(A.slevel); f(A.srowptr);
+  f(A.srows); f(A.pofs); f(A.level_ptr); f(A.level_list); f(A.ch_ptr); f(A.ch_list); f(A.relofs);
+  f(A.uofs); f(A.vofs); f(A.relmap); f(A.kmap); f(A.wt_ptr); f(A.wt_idx); f(A.dslot); f(A.jt_ptr);
+  f(A.jt_a); f(A.jt_b); f(A.jt_r); f(A.gt_ptr); f(A.gt_e); f(A.gt_r); f(A.ht_ptr); f(A.ht_e); f(A.ht_r);
+  f(A.g_col2); f(A.h_col2); f(A.w_row2); f(A.w_col2);
+}
+
+struct BlobHeader {
+  char magic[8];
+  uint32_t version, user_perm;
+  uint64_t hash;
+  int32_t leaf, n, me, mi, ns, nlevels;
+  int64_t nnz_l;
+  double flops;
+  int32_t nrelax[3], max_width;
+  double zrelax[3];
+};
+}  // namespace
+
+uint64_t pattern_hash(const Pattern& p) {
+  uint64_t h = 1469598103934665603ull;  // FNV-1a over the dimensions and the index arrays
+  auto mix = [&](const void* d, size_t bytes) {
+    const unsigned char* c = static_cast<const unsigned char*>(d);
+    for (size_t i = 0; i < bytes; ++i) { h ^= c[i]; h *= 1099511628211ull; }
+  };
+  const int32_t dims[3] = {p.n, p.me, p.mi};
+  mix(dims, sizeof(dims));
+  for (const std::vector<int32_t>* v : {&p.w_row, &p.w_col, &p.g_rowptr, &p.g_col, &p.h_rowptr, &p.h_col}) {
+    const uint64_t len = v->size();
+    mix(&len, sizeof(len));
+    if (len) mix(v->data(), len * sizeof(int32_t));
+  }
+  return h;
+}
+
+size_t analysis_blob_size(const Analysis& A0) {
+  Analysis& A = const_cast<Analysis&>(A0);  // for_each_array only reads here
+  size_t total = sizeof(BlobHeader);
+  for_each_array(A, [&](auto& v) { total += sizeof(uint64_t) + v.size() * sizeof(v[0]); });
+  return total;
+}
+
+void save_analysis(const Analysis& A0, int leaf, bool user_perm, char* out) {
+  Analysis& A = const_cast<Analysis&>(A0);  // for_each_array only reads here
+  const AmalgamationParams& ap = amalgamation_params();
+  BlobHeader h{};
+  std::memcpy(h.magic, kMagic, 8);
+  h.version = kVersion;
+  h.user_perm = user_perm ? 1u : 0u;
+  h.hash = pattern_hash(A.pat);
+  h.leaf = leaf;
+  h.n = A.n;
+  h.me = A.pat.me;
+  h.mi = A.pat.mi;
+  h.ns = A.ns;
+  h.nlevels = A.nlevels;
+  h.nnz_l = A.nnz_l;
+  h.flops = A.flops;
+  h.nrelax[0] = ap.enabled ? ap.nrelax0 : -1;
+  h.nrelax[1] = ap.nrelax1;
+  h.nrelax[2] = ap.nrelax2;
+  h.max_width = ap.max_width;
+  h.zrelax[0] = ap.zrelax0;
+  h.zrelax[1] = ap.zrelax1;
+  h.zrelax[2] = ap.zrelax2;
+  char* o = out;
+  std::memcpy(o, &h, sizeof(h));
+  o += sizeof(h);
+  for_each_array(A, [&](auto& v) {
+    const uint64_t len = v.size();
+    std::memcpy(o, &len, sizeof(len));
+    o += sizeof(len);
+    if (len) std::memcpy(o, v.data(), len * sizeof(v[0]));
+    o += len * sizeof(v[0]);
+  });
+}
+
+std::string load_analysis(const Pattern& p, int leaf, bool user_perm, const char* blob, size_t size, Analysis& A,
+                          int& code) {
+  code = CKKT_INVALID_ARG;
+  BlobHeader h;
+  if (!blob || size < sizeof(h)) return "blob too small";
+  std::memcpy(&h, blob, sizeof(h));
+  const AmalgamationParams& ap = amalgamation_params();
+  if (std::memcmp(h.magic, kMagic, 8) != 0 || h.version != kVersion) return "not a ckkt analysis blob of this version";
+  if (h.n != p.n || h.me != p.me || h.mi != p.mi || h.leaf != leaf || h.user_perm != (user_perm ? 1u : 0u) ||
+      h.hash != pattern_hash(p))
+    return "blob was analysed for another pattern or ordering";
+  if (h.nrelax[0] != (ap.enabled ? ap.nrelax0 : -1) || h.nrelax[1] != ap.nrelax1 || h.nrelax[2] != ap.nrelax2 ||
+      h.max_width != ap.max_width || h.zrelax[0] != ap.zrelax0 || h.zrelax[1] != ap.zrelax1 || h.zrelax[2] != ap.zrelax2)
+    return "blob was analysed with other amalgamation parameters";
+  const char* o = blob + sizeof(h);
+  const char* e = blob + size;
+  bool ok = true;
+  for_each_array(A, [&](auto& v) {
+    uint64_t len = 0;
+    if (!ok || o + sizeof(len) > e) { ok = false; return; }
+    std::memcpy(&len, o, sizeof(len));
+    o += sizeof(len);
+    const size_t bytes = len * sizeof(v[0]);
+    if (len > size || o + bytes > e) { ok = false; return; }
+    v.resize(len);
+    if (len) std::memcpy(v.data(), o, bytes);
+    o += bytes;
+  });
+  if (!ok || o != e) return "truncated or corrupt analysis blob";
+  A.pat = p;
+  A.n = p.n;
+  A.ns = h.ns;
+  A.nlevels = h.nlevels;
+  A.nnz_l = h.nnz_l;
+  A.flops = h.flops;
+  if ((int)A.perm.size() != p.n || (int)A.sfirst.size() != A.ns + 1 || (int)A.kp.size() != p.n + 1)
+    return "inconsistent analysis blob";
+  code = CKKT_OK;
   return "";
 }
 

@@ -75,6 +75,17 @@ const AmalgamationParams& amalgamation_params();
 // Returns "" on success, else an error message; code receives a ckkt_status value.
 std::string analyze(const Pattern& p, int leaf, const int32_t* user_perm, Analysis& A, int& code);
 
+// Serialized analysis (the symbolic analysis depends on the pattern only and can be computed
+// once, offline, and reused).  The blob starts with a header (magic, version, the pattern's FNV-1a hash,
+// leaf, whether a caller ordering was used, amalgamation parameters) followed by every array of the
+// Analysis except the pattern itself, which load_analysis takes from the caller and checks by hash.
+uint64_t pattern_hash(const Pattern& p);
+size_t analysis_blob_size(const Analysis& A);
+void save_analysis(const Analysis& A, int leaf, bool user_perm, char* out);  // out: analysis_blob_size bytes
+// Returns "" on success; code receives CKKT_INVALID_ARG for a blob of another pattern / settings.
+std::string load_analysis(const Pattern& p, int leaf, bool user_perm, const char* blob, size_t size, Analysis& A,
+                          int& code);
+
 // Exact L pattern for the exported ordering (computed on demand).
 void export_l_pattern(const Analysis& A, std::vector<int64_t>& Lp, std::vector<int32_t>& Li);
 

@@ -732,6 +732,7 @@ T* upload(const std::vector<T>& v, std::vector<void*>& owned, int64_t& bytes) {
 struct ckkt_ctx {
   ckkt::Analysis A;
   ckkt_options opt{};
+  bool user_perm = false;  // the ordering came from the caller (options.perm)
   int B = 1;
   bool has_device = false;
   cudaStream_t stream = nullptr;
@@ -1081,12 +1082,9 @@ ckkt_status setup_device(ckkt_ctx* c) {
         for (int s2 : q) place(s2);
         for (int s2 : tq) place(s2);
         if (off != A.pofs[ns]) return CKKT_INVALID_ARG;  // every supernode placed exactly once
-        for (int s2 = 0; s2 < ns; ++s2) {
-          A.pofs[s2] = np[s2];
-          c->meta_h[s2].pofs = np[s2];
-        }
-        CK(cudaMemcpy(const_cast<int64_t*>(c->S.pofs), A.pofs.data(), sizeof(int64_t) * A.pofs.size(),
-                      cudaMemcpyHostToDevice));
+        np[ns] = off;
+        for (int s2 = 0; s2 < ns; ++s2) c->meta_h[s2].pofs = np[s2];  // (A.pofs stays canonical: blobs)
+        CK(cudaMemcpy(const_cast<int64_t*>(c->S.pofs), np.data(), sizeof(int64_t) * np.size(), cudaMemcpyHostToDevice));
         CK(cudaMemcpy(const_cast<SnMeta*>(c->S.meta), c->meta_h.data(), sizeof(SnMeta) * ns, cudaMemcpyHostToDevice));
         std::vector<SnMeta> tm(sn.size());
         for (size_t k = 0; k < sn.size(); ++k) {
@@ -1357,7 +1355,34 @@ void ckkt_destroy(ckkt_ctx* c) {
   delete c;
 }
 
+static ckkt_status setup_impl(const ckkt_pattern* p, const ckkt_options* opt, const void* blob, int64_t blob_size,
+                              ckkt_ctx** out);
+
 ckkt_status ckkt_setup(const ckkt_pattern* p, const ckkt_options* opt, ckkt_ctx** out) {
+  return setup_impl(p, opt, nullptr, 0, out);
+}
+
+ckkt_status ckkt_setup_from_analysis(const ckkt_pattern* p, const ckkt_options* opt, const void* blob, int64_t size,
+                                     ckkt_ctx** out) {
+  if (!blob || size <= 0) return CKKT_INVALID_ARG;
+  return setup_impl(p, opt, blob, size, out);
+}
+
+ckkt_status ckkt_export_analysis(const ckkt_ctx* c, void* buf, int64_t* size) {
+  if (!c || !size) return CKKT_INVALID_ARG;
+  const int64_t need = (int64_t)ckkt::analysis_blob_size(c->A);
+  if (!buf) {
+    *size = need;
+    return CKKT_OK;
+  }
+  if (*size < need) return CKKT_INVALID_ARG;
+  ckkt::save_analysis(c->A, c->opt.leaf > 0 ? c->opt.leaf : 64, c->user_perm, static_cast<char*>(buf));
+  *size = need;
+  return CKKT_OK;
+}
+
+static ckkt_status setup_impl(const ckkt_pattern* p, const ckkt_options* opt, const void* blob, int64_t blob_size,
+                              ckkt_ctx** out) {
   if (!p || !out) return CKKT_INVALID_ARG;
   *out = nullptr;
   ckkt_options o;
@@ -1398,8 +1423,14 @@ ckkt_status ckkt_setup(const ckkt_pattern* p, const ckkt_options* opt, ckkt_ctx*
     pat.h_rowptr.assign(1, 0);
   }
   int code = 0;
-  std::string err = ckkt::analyze(pat, o.leaf > 0 ? o.leaf : 64, o.perm, c->A, code);
+  const int leaf = o.leaf > 0 ? o.leaf : 64;
+  std::string err = blob ? ckkt::load_analysis(pat, leaf, o.perm != nullptr, static_cast<const char*>(blob),
+                                               (size_t)blob_size, c->A, code)
+                         : ckkt::analyze(pat, leaf, o.perm, c->A, code);
   if (!err.empty()) return (ckkt_status)code;
+  if (blob && o.perm && !std::equal(c->A.perm.begin(), c->A.perm.end(), o.perm)) return CKKT_INVALID_ARG;
+  c->opt.perm = nullptr;  // (the caller's array is not referenced after setup; remembered as a flag)
+  c->user_perm = o.perm != nullptr;
   c->n = p->n;
   c->me = p->m_e;
   c->mi = p->m_i;

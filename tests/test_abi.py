@@ -163,3 +163,49 @@ def test_elimination_order_is_a_postorder_of_perm():
     o = OK.SparseKKT(pat.n, pat.m, 0, pat.w_row, pat.w_col, pat.j_rowptr, pat.j_col, E32, E32[:0], perm=order)
     assert len(o.Li) == len(Li)
     assert ckkt.lib().ckkt_export_elimination_order(ctx.h, None) == ckkt.CKKT_INVALID_ARG
+
+
+def test_analysis_blob_round_trip():
+    """NEXT-2 (the analysis can be done offline): a context set up from an exported analysis
+    has exactly the arrays of a freshly analysed one; a blob of another pattern, leaf or ordering is
+    refused; a truncated blob is refused."""
+    pat = dist.build_pattern(40)
+    args = (pat.n, pat.m, 0, pat.w_row, pat.w_col, pat.j_rowptr, pat.j_col, None, None)
+    ctx = _host_ctx(*args, leaf=64)
+    blob = ctx.export_analysis()
+    assert len(blob) > 1000
+    ctx2 = _host_ctx(*args, leaf=64, analysis=blob)
+    a, b = ctx.export_symbolic(), ctx2.export_symbolic()
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+    assert np.array_equal(ctx.export_elimination_order(), ctx2.export_elimination_order())
+    assert ctx.get_sizes() == ctx2.get_sizes()
+    assert np.array_equal(ctx2.export_analysis(), blob)
+    for bad in (dict(leaf=65, analysis=blob), dict(leaf=64, analysis=blob[:-8]), dict(leaf=64, analysis=np.full(64, 7, np.uint8))):
+        with pytest.raises(ckkt.CKKTError) as e:
+            _host_ctx(*args, **bad)
+        assert e.value.code == ckkt.CKKT_INVALID_ARG
+    other = dist.build_pattern(41)
+    with pytest.raises(ckkt.CKKTError):
+        _host_ctx(other.n, other.m, 0, other.w_row, other.w_col, other.j_rowptr, other.j_col, None, None, leaf=64,
+                  analysis=blob)
+    perm = np.arange(pat.n, dtype=np.int32)[::-1].copy()
+    with pytest.raises(ckkt.CKKTError):  # blob of the built-in ordering used with a caller ordering
+        _host_ctx(*args, leaf=64, perm=perm, analysis=blob)
+
+
+@pytest.mark.parametrize("N,leaf", [(1500, 64), (2500, 1072)])
+def test_parallel_analysis_matches_oracle_and_thread_count(N, leaf, monkeypatch):
+    """The multithreaded analysis (parallel nested-dissection levels, leaf minimum degree, pattern and map
+    construction) reproduces the specified ordering and symbolic arrays exactly: against the oracle, and
+    with one thread against many."""
+    pat = dist.build_pattern(N)
+    args = (pat.n, pat.m, 0, pat.w_row, pat.w_col, pat.j_rowptr, pat.j_col, None, None)
+    many = _host_ctx(*args, leaf=leaf)
+    monkeypatch.setenv("CKKT_THREADS", "1")
+    one = _host_ctx(*args, leaf=leaf)
+    assert np.array_equal(many.export_analysis(), one.export_analysis())
+    perm, parent, cc, Lp, Li = many.export_symbolic()
+    o = OK.SparseKKT(pat.n, pat.m, 0, pat.w_row, pat.w_col, pat.j_rowptr, pat.j_col, E32, E32[:0], leaf=leaf)
+    assert np.array_equal(perm, o.perm) and np.array_equal(parent, o.parent) and np.array_equal(cc, o.colcount)
+    assert np.array_equal(Lp, o.Lp) and np.array_equal(Li, o.Li)
