@@ -84,25 +84,36 @@ struct NDGraph {
   std::atomic<int32_t>* tags;
   int tag() const { return tags->fetch_add(1) + 1; }
 
-  // BFS level sets of G[label == lab] from r; each level sorted ascending.
-  void bfs(int lab, int r, std::vector<std::vector<int32_t>>& levels) const {
-    levels.clear();
+  // BFS level sets of G[label == lab] from r, flat: level l = verts[lev[l] .. lev[l+1]), each sorted
+  // ascending (one allocation per BFS instead of one per level)
+  struct Levels {
+    std::vector<int32_t> verts;
+    std::vector<int64_t> lev;
+    int count() const { return (int)lev.size() - 1; }
+    int64_t size(int l) const { return lev[l + 1] - lev[l]; }
+  };
+  void bfs(int lab, int r, Levels& L) const {
+    L.verts.clear();
+    L.lev.assign(1, 0);
     const int ver = tag();
-    std::vector<int32_t> cur{r}, nxt;
     visit[r] = ver;
-    while (!cur.empty()) {
-      nxt.clear();
-      for (int v : cur)
+    L.verts.push_back(r);
+    int64_t b = 0;
+    while (b < (int64_t)L.verts.size()) {
+      const int64_t e = (int64_t)L.verts.size();
+      for (int64_t q = b; q < e; ++q) {
+        const int v = L.verts[q];
         for (int p = xadj[v]; p < xadj[v + 1]; ++p) {
           const int a = adj[p];
           if (ald(label + a) == lab && visit[a] != ver) {
             visit[a] = ver;
-            nxt.push_back(a);
+            L.verts.push_back(a);
           }
         }
-      std::sort(cur.begin(), cur.end());
-      levels.push_back(cur);
-      cur.swap(nxt);
+      }
+      std::sort(L.verts.begin() + b, L.verts.begin() + e);
+      L.lev.push_back(e);
+      b = e;
     }
   }
 
@@ -147,30 +158,31 @@ struct NDGraph {
   bool split(const std::vector<int32_t>& C, std::vector<int32_t>& S, std::vector<std::vector<int32_t>>& comps) const {
     const int lab = tag();
     for (int v : C) ast(label + v, lab);
-    std::vector<std::vector<int32_t>> lev, lev2;
+    Levels lev, lev2;
     bfs(lab, C[0], lev);
     for (;;) {  // pseudo-peripheral vertex (George-Liu)
-      const auto& last = lev.back();
+      const int nl = lev.count();
       int x = -1, xd = 0;
-      for (int v : last) {  // ascending; strict improvement keeps the smaller index on ties
+      for (int64_t q = lev.lev[nl - 1]; q < lev.lev[nl]; ++q) {  // last level, ascending; strict improvement
+        const int v = lev.verts[q];                             // keeps the smaller index on ties
         const int d = deg_in(lab, v);
         if (x < 0 || d < xd) { x = v; xd = d; }
       }
       bfs(lab, x, lev2);
-      if (lev2.size() > lev.size()) lev.swap(lev2);
+      if (lev2.count() > lev.count()) std::swap(lev, lev2);
       else break;
     }
-    const int h = (int)lev.size() - 1;
+    const int h = lev.count() - 1;
     if (h < 2) return false;
     const int ilo = std::max(1, h / 3), ihi = std::min(h - 1, h - h / 3);
     int bi = -1;
     for (int i = ilo; i <= ihi; ++i) {
       if (bi < 0) { bi = i; continue; }
-      const size_t sz = lev[i].size(), bsz = lev[bi].size();
+      const int64_t sz = lev.size(i), bsz = lev.size(bi);
       const int c = std::abs(2 * i - h), bc = std::abs(2 * bi - h);
       if (sz < bsz || (sz == bsz && c < bc)) bi = i;
     }
-    S = lev[bi];
+    S.assign(lev.verts.begin() + lev.lev[bi], lev.verts.begin() + lev.lev[bi + 1]);
     std::vector<int32_t> rest;
     rest.reserve(C.size() - S.size());
     std::set_difference(C.begin(), C.end(), S.begin(), S.end(), std::back_inserter(rest));
