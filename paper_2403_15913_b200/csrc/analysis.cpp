@@ -667,7 +667,7 @@ std::string analyze(const Pattern& p, int leaf, const int32_t* user_perm, Analys
     }
     // final supernodes: groups split into chunks of at most MAXW columns (a chunk's rows are the
     // suffix of the group's rows starting at its first column; chunk k's parent is chunk k+1)
-    constexpr int MAXW = 64;
+    const int MAXW = std::max(1, std::min(64, P.max_width));  // (amalgamation parameter; 64 by default)
     std::vector<int32_t> sf, stopf;  // first column, top fundamental supernode of the owning group
     for (size_t g = 0; g < gfirst.size(); ++g) {
       const int gend = fsfirst[gtop[g] + 1];
