@@ -76,7 +76,8 @@ typedef struct {
   double gamma;                /* HyKKT augmentation, default 1e7; ignored by Lifted */
   double cg_rtol;              /* CG stop ||r_k||_2 <= cg_rtol ||b||_2, default 1e-10 (reading R6); finite, > 0 */
   int32_t cg_maxit;            /* default 200 */
-  double ref_tol;              /* refinement stop on the componentwise backward error, default 1e-14 (R7) */
+  double ref_tol;              /* refinement stop on the componentwise backward error, default 1e-10 (R7:
+                                  the north-star relative KKT residual) */
   int32_t ref_maxit;           /* default 10; 0 = no refinement */
   int32_t batch;               /* B >= 1 independent instances sharing the pattern */
   int32_t leaf;                /* nested-dissection leaf size, default 64 */

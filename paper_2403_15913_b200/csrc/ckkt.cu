@@ -1315,7 +1315,7 @@ void ckkt_default_options(ckkt_options* o) {
   o->cg_rtol = 1e-10;
   o->cg_rtol_corr = 1e-6;
   o->cg_maxit = 200;
-  o->ref_tol = 1e-14;
+  o->ref_tol = 1e-10;  // the north-star bar on the relative KKT residual (reading R7)
   o->ref_maxit = 10;
   o->batch = 1;
   o->leaf = 64;
