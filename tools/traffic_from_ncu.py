@@ -15,8 +15,11 @@ for row in r[2:]:
     per.setdefault(name, tot)  # first capture of each kernel
 fwd = per['k_fwd_tiny'] + per['k_fwd_persist'] + per.get('k_fwd_top', 0.0)
 bwd = per.get('k_bwd_top', 0.0) + per['k_bwd_persist'] + per['k_bwd_tiny']
+fac = per.get('k_factor_tiny', 0.0) + per['k_factor_persist']
 res = {"_source": note, "k_fwd_tiny + k_fwd_persist + k_fwd_top (one forward sweep)": fwd,
-       "k_bwd_top + k_bwd_persist + k_bwd_tiny (one backward sweep)": bwd, "k_factor_persist": per['k_factor_persist'],
+       "k_bwd_top + k_bwd_persist + k_bwd_tiny (one backward sweep)": bwd,
+       "k_factor_tiny + k_factor_persist (one numeric factorization)": fac,
+       "k_condense": next((v for k, v in per.items() if k.startswith('k_condense')), None),
        "_per_kernel": per}
 json.dump(res, open('profiles/traffic.json', 'w'), indent=1)
 print(json.dumps(res, indent=1))
