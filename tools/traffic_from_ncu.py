@@ -19,7 +19,7 @@ fac = per.get('k_factor_tiny', 0.0) + per['k_factor_persist']
 res = {"_source": note, "k_fwd_tiny + k_fwd_persist + k_fwd_top (one forward sweep)": fwd,
        "k_bwd_top + k_bwd_persist + k_bwd_tiny (one backward sweep)": bwd,
        "k_factor_tiny + k_factor_persist (one numeric factorization)": fac,
-       "k_condense": next((v for k, v in per.items() if k.startswith('k_condense')), None),
+       "k_condense": next((v for k, v in per.items() if "k_condense" in k), None),
        "_per_kernel": per}
 json.dump(res, open('profiles/traffic.json', 'w'), indent=1)
 print(json.dumps(res, indent=1))
