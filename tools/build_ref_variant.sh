@@ -1,7 +1,7 @@
 #!/bin/bash
 # usage: tools/build_ref_variant.sh <name> <git-ref> ["<-D flags>"]  -> build_variants/<name>/libckkt.so
 set -e -o pipefail
-cd /root/repo
+cd "$(dirname "$0")/.."
 d=build_variants/src_$1
 rm -rf $d; mkdir -p $d/x/csrc $d/include build_variants/$1
 for f in ckkt.cu mf_kernels.cuh dense_front.cuh analysis.h analysis.cpp; do git show $2:paper_2403_15913_b200/csrc/$f > $d/x/csrc/$f; done

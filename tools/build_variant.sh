@@ -1,7 +1,7 @@
 #!/bin/bash
 # usage: tools/build_variant.sh <name> "<-D flags>"  -> build_variants/<name>/libckkt.so (experiments only)
 set -e
-cd /root/repo
+cd "$(dirname "$0")/.."
 mkdir -p build_variants/$1
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 -Xptxas -O3 \
   --expt-relaxed-constexpr -I include $2 -c paper_2403_15913_b200/csrc/ckkt.cu -o build_variants/$1/ckkt.o

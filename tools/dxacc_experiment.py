@@ -2,7 +2,7 @@
 CG (no separate dx solve) vs the fresh solve dx = K^{-1}(-r_gamma - G^T dy); refinement counts."""
 import sys
 import numpy as np
-sys.path.insert(0, '/root/repo'); sys.path.insert(0, '/root/repo/tests')
+sys.path.insert(0, __import__('os').path.dirname(__import__('os').path.dirname(__import__('os').path.abspath(__file__)))); sys.path.insert(0, __import__('os').path.join(__import__('os').path.dirname(__import__('os').path.dirname(__import__('os').path.abspath(__file__))), 'tests'))
 from oracle import kkt as OK
 from kkt_cases import distillation_case, E32
 

@@ -2,7 +2,7 @@
 projected onto the first pass's Krylov directions (Init-CG / deflation) vs the plain x0 = 0."""
 import sys
 import numpy as np
-sys.path.insert(0, '/root/repo'); sys.path.insert(0, '/root/repo/tests')
+sys.path.insert(0, __import__('os').path.dirname(__import__('os').path.dirname(__import__('os').path.abspath(__file__)))); sys.path.insert(0, __import__('os').path.join(__import__('os').path.dirname(__import__('os').path.dirname(__import__('os').path.abspath(__file__))), 'tests'))
 from oracle import kkt as OK
 from kkt_cases import distillation_case, E32
 
