@@ -69,6 +69,25 @@ struct Sched {
   int small_panel;                // doubles per warp of a small front's shared-memory panel
 };
 
+// -DCKKT_BOUNDS (tools/build_variant.sh bounds "-DCKKT_BOUNDS"): every panel / update-matrix /
+// update-vector / solution access region of every supernode, and every extend-add target, is checked
+// against its array before use; a violation prints and traps.  The checked build is what stands in for
+// compute-sanitizer (closed on this GPU pool); release builds compile the checks away.
+#ifdef CKKT_BOUNDS
+#define CKB(cond)                                                                              \
+  do {                                                                                         \
+    if (!(cond)) {                                                                             \
+      printf("ckkt bounds: %s failed (%s:%d, block %d thread %d)\n", #cond, __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)threadIdx.x);                                                 \
+      __trap();                                                                                \
+    }                                                                                          \
+  } while (0)
+#else
+#define CKB(cond) \
+  do {            \
+  } while (0)
+#endif
+
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -190,6 +209,7 @@ __device__ __forceinline__ void extend_add(const double* __restrict__ Uc, int mc
         sv[q] = ok ? __ldcg(Uc + i + (int64_t)j * mc) : 0.0;
         if (ok) {
           const int ri = __ldg(rel + i);
+          CKB(ri >= rj[q] && ri < w + mu && (PART == 0 ? rj[q] < w : rj[q] >= w));
           tgt[q] = PART == 0 ? ri + rj[q] * ldp : (ri - w) + (rj[q] - w) * mu;
         } else {
           tgt[q] = -1;
@@ -246,12 +266,17 @@ __device__ void factor_small(const SymDev& S, int s, int b, int tid, double* Ps,
   const int mu = m - w, ldp = m;
   double* P = L + b * Lsize + S.pofs[s];
   double* U = Ub + b * Usize + S.uofs[s];
+  CKB(S.pofs[s] + (int64_t)m * w <= Lsize && S.uofs[s] + (int64_t)mu * mu <= Usize && m * w <= SMALL_PANEL_MAX);
   for (int i = tid; i < m * w; i += nt) Ps[i] = 0.0;
   __syncwarp();
-  for (int64_t k = S.kp[f] + tid; k < S.kp[f + w]; k += nt) Ps[S.kmap[k]] = Kb[k];
+  for (int64_t k = S.kp[f] + tid; k < S.kp[f + w]; k += nt) {
+    CKB(S.kmap[k] >= 0 && S.kmap[k] < m * w);
+    Ps[S.kmap[k]] = Kb[k];
+  }
   __syncwarp();
   for (int ci = S.ch_ptr[s]; ci < S.ch_ptr[s + 1]; ++ci) {
     const int c = S.ch_list[ci];
+    CKB(S.uofs[c] + (int64_t)off_rows(S, c) * off_rows(S, c) <= Usize);
     extend_add<0>(Ub + b * Usize + S.uofs[c], off_rows(S, c), S.relw[c], S.relmap + S.relofs[c], w, Ps, ldp, U,
                   mu, tid, nt);
     __syncwarp();
@@ -282,18 +307,21 @@ __device__ void factor_big(const SymDev& S, int s, int b, double* Ps, double* ds
   const int mp = (m + 7) & ~7, wp = (w + 3) & ~3, ldp = mp;
   double* P = L + b * Lsize + S.pofs[s];
   double* U = Ub + b * Usize + S.uofs[s];
+  CKB(S.pofs[s] + (int64_t)m * w <= Lsize && S.uofs[s] + (int64_t)mu * mu <= Usize && w <= 64);
   unsigned long long* ph = (g_debug_ph && b == 0 && tid == 0) ? g_debug_ph + 8 * (int64_t)s : nullptr;
   if (ph) ph[0] = gtimer();
   for (int i = tid; i < mp * wp + 8; i += nt) Ps[i] = 0.0;
   __syncthreads();
   for (int64_t k = S.kp[f] + tid; k < S.kp[f + w]; k += nt) {
     const int q = S.kmap[k];
+    CKB(q >= 0 && q < m * w);
     Ps[(q % m) + (q / m) * mp] = Kb[k];
   }
   __syncthreads();
   if (ph) ph[1] = gtimer();
   for (int ci = S.ch_ptr[s]; ci < S.ch_ptr[s + 1]; ++ci) {
     const int c = S.ch_list[ci];
+    CKB(S.uofs[c] + (int64_t)off_rows(S, c) * off_rows(S, c) <= Usize);
     extend_add<0>(Ub + b * Usize + S.uofs[c], off_rows(S, c), S.relw[c], S.relmap + S.relofs[c], w, Ps, ldp, U,
                   mu, tid, nt);
     __syncthreads();
@@ -549,7 +577,11 @@ __device__ __forceinline__ void warp_gather_children(const SymDev& S, const Swee
       const ChMeta cm = cmeta[k];
       const double* uc = Vb + cm.vofs;
       const int32_t* rel = S.relmap + cm.relofs;
-      for (int i = lane; i < cm.mc; i += LW) v[__ldg(rel + i)] += __ldcg(uc + i);
+      CKB(cm.vofs + cm.mc <= A.Vsize);
+      for (int i = lane; i < cm.mc; i += LW) {
+        CKB(__ldg(rel + i) >= 0 && __ldg(rel + i) < M.m);
+        v[__ldg(rel + i)] += __ldcg(uc + i);
+      }
       wsync();
     }
   }
@@ -561,6 +593,7 @@ __device__ __forceinline__ void fwd_warp_step(const SymDev& S, const SweepArgs& 
   double* x = A.X + (int64_t)b * A.n;
   const int f = M.f, w = M.w, m = M.m, mu = m - w;
   const double* P = A.L + b * A.Lsize + M.pofs;
+  CKB(M.pofs + (int64_t)m * w <= A.Lsize && M.vofs + mu <= A.Vsize && f + w <= A.n && m <= A.max_m);
   if (lane == 0) prefetch_l2(P, 8ll * m * w);  // the panel streams into L2 while the children are gathered
   const unsigned long long t0 = g_debug_ts ? gtimer() : 0ull;
   for (int i = lane; i < m; i += LW) v[i] = (i < w) ? x[f + i] : 0.0;
@@ -639,9 +672,13 @@ __device__ __forceinline__ void bwd_warp_step(const SymDev& S, const SweepArgs& 
   double* x = A.X + (int64_t)b * A.n;
   const int f = M.f, w = M.w, m = M.m, mu = m - w;
   const double* P = A.L + b * A.Lsize + M.pofs;
+  CKB(M.pofs + (int64_t)m * w <= A.Lsize && f + w <= A.n && m <= A.max_m);
   if (lane == 0) prefetch_l2(P, 8ll * m * w);  // independent of the parent: overlap with the wait
   for (int i = lane; i < w; i += LW) tv[i] = x[f + i];
-  for (int i = lane; i < mu; i += LW) ridx[i] = __ldg(S.srows + M.r0 + w + i);
+  for (int i = lane; i < mu; i += LW) {
+    ridx[i] = __ldg(S.srows + M.r0 + w + i);
+    CKB(ridx[i] >= f + w && ridx[i] < A.n);
+  }
   const unsigned long long t0 = g_debug_ts ? gtimer() : 0ull;
   if (p >= 0) wait_epoch(done + p, A.epoch);  // all lanes: uniform control flow
   wsync();
@@ -805,6 +842,7 @@ __global__ void __launch_bounds__(TOP_THREADS, TOP_MINB) k_fwd_top(SymDev S, Swe
     const int s = M.pad1, f = M.f, w = M.w, m = M.m, mu = m - w;
     int* done = A.done_all + (int64_t)b * A.ns;
     const bool sk = A.skip && A.skip[b];
+    CKB(M.pofs + (int64_t)m * w <= A.Lsize && M.vofs + mu <= A.Vsize && f + w <= A.n && m <= A.max_m && w <= 64);
     const unsigned long long t0 = g_debug_ts ? gtimer() : 0ull;
     unsigned long long t1 = t0;
     const double* Pl = sk ? nullptr : top_panel(A, M, b, buf, sh, tid == 0);
@@ -836,6 +874,7 @@ __global__ void __launch_bounds__(TOP_THREADS, TOP_MINB) k_fwd_top(SymDev S, Swe
               if (tid < cm.mc) {
                 rl[k] = __ldg(S.relmap + cm.relofs + tid);
                 uv[k] = __ldcg(Vb + cm.vofs + tid);
+                CKB(rl[k] >= 0 && rl[k] < m && cm.vofs + cm.mc <= A.Vsize);
               }
             }
           }
