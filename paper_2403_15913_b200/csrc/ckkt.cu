@@ -931,8 +931,11 @@ ckkt_status setup_device(ckkt_ctx* c) {
   }
   {  // factor tasks in level order (tiny supernodes excluded): big supernodes (one CTA) and bundles of
      // small ones (one warp each)
-    std::vector<int32_t> tsn, tbig;
+    std::vector<int32_t> tsn, tbig, tptr{0};
     c->big_smem = 0;
+    int dev_sms0 = 148;
+    CK(cudaDeviceGetAttribute(&dev_sms0, cudaDevAttrMultiProcessorCount, c->opt.device));
+    const int64_t chunk_max = getenv("CKKT_CHUNK") ? std::max(1, atoi(getenv("CKKT_CHUNK"))) : 32;  // tuning only
     // many supernodes: more one-warp fronts keep 8 independent fronts in flight per CTA (C3: -2 ms per
     // refactor); few supernodes: the CTA path finishes the short critical path sooner (C2)
     c->small_panel = ((int64_t)A.ns * B > 200000) ? SMALL_PANEL_MAX : SMALL_PANEL_MIN;
@@ -948,20 +951,25 @@ ckkt_status setup_device(ckkt_ctx* c) {
         } else {
           tbig.push_back(1);
           tsn.push_back(s);
-          for (int q = 1; q < SMALL_WARPS; ++q) tsn.push_back(-1);
+          tptr.push_back((int32_t)tsn.size());
           const int64_t mp = (m + 7) & ~7, wp = (w + 3) & ~3;
           c->big_smem = std::max<int64_t>(c->big_smem, 8 * (mp * wp + 8));
         }
       }
-      for (size_t k = 0; k < small.size(); k += SMALL_WARPS) {
+      // one-warp fronts of this level in chunks of SMALL_WARPS..chunk_max (about four chunks per SM)
+      const int64_t csz = std::max<int64_t>(SMALL_WARPS, std::min<int64_t>(chunk_max, (int64_t)small.size() * B /
+                                                                                         (4 * (int64_t)dev_sms0)));
+      for (size_t k = 0; k < small.size(); k += csz) {
         tbig.push_back(0);
-        for (int q = 0; q < SMALL_WARPS; ++q) tsn.push_back(k + q < small.size() ? small[k + q] : -1);
+        for (size_t q = k; q < std::min(small.size(), k + (size_t)csz); ++q) tsn.push_back(small[q]);
+        tptr.push_back((int32_t)tsn.size());
       }
     }
     c->ntask = (int)tbig.size();
-    int32_t *d_tsn, *d_tbig;
+    int32_t *d_tsn, *d_tbig, *d_tptr;
     UP(d_tsn, tsn);
     UP(d_tbig, tbig);
+    UP(d_tptr, tptr);
     std::vector<int32_t> zeros((size_t)B * A.ns, 0), z2(4, 0);
     int32_t *dfac, *dfwd, *dbwd, *cfac, *cfwd, *cbwd;
     UP(dfac, zeros);
@@ -970,9 +978,9 @@ ckkt_status setup_device(ckkt_ctx* c) {
     UP(cfac, z2);
     UP(cfwd, z2);
     UP(cbwd, z2);
-    c->Qfac = Sched{c->ntask, d_tsn, d_tbig, dfac, cfac, c->small_panel};
-    c->Qfwd = Sched{c->ntask, d_tsn, d_tbig, dfwd, cfwd, c->small_panel};
-    c->Qbwd = Sched{c->ntask, d_tsn, d_tbig, dbwd, cbwd, c->small_panel};
+    c->Qfac = Sched{c->ntask, d_tsn, d_tbig, d_tptr, dfac, cfac, c->small_panel};
+    c->Qfwd = Sched{c->ntask, d_tsn, d_tbig, d_tptr, dfwd, cfwd, c->small_panel};
+    c->Qbwd = Sched{c->ntask, d_tsn, d_tbig, d_tptr, dbwd, cbwd, c->small_panel};
     c->fac_smem = std::max<int64_t>(c->big_smem, 8 * SMALL_WARPS * c->small_panel);
     c->sol_smem = 8 * ((int64_t)SOLVE_WORKERS * (c->max_m + 64 + RED_SZ)) +
                   4 * (int64_t)SOLVE_WORKERS * c->max_m;  // + per-worker row indices (backward)

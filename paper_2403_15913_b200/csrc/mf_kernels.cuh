@@ -62,8 +62,9 @@ struct SymDev {
 
 struct Sched {
   int ntask;                      // tasks per instance
-  const int32_t* task_sn;         // [ntask * SMALL_WARPS], -1 = empty slot; big task uses slot 0
-  const int32_t* task_big;        // [ntask]
+  const int32_t* task_sn;         // fronts of task t: task_sn[task_ptr[t] .. task_ptr[t+1])
+  const int32_t* task_big;        // [ntask]: 1 = one front for the whole CTA, 0 = a chunk of one-warp fronts
+  const int32_t* task_ptr;        // [ntask + 1]
   int* done;                      // [B * ns] epoch flags
   int* ctr;                       // [2] ticket counters (alternating per epoch)
   int small_panel;                // doubles per warp of a small front's shared-memory panel
@@ -350,6 +351,8 @@ __global__ void __launch_bounds__(MF_THREADS)
   extern __shared__ double smem[];  // max(big panel, SMALL_WARPS small panels)
   __shared__ double dsh_all[SMALL_WARPS][64];  // reciprocal pivots (per warp; the CTA path uses row 0)
   __shared__ int tk;
+  __shared__ int chunk_ctr;
+  if (threadIdx.x == 0) chunk_ctr = 0;
   if (blockIdx.x == 0 && threadIdx.x == 0) Q.ctr[(epoch + 1) & 1] = 0;  // slot of the next launch
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int total = Q.ntask * B;
@@ -360,7 +363,7 @@ __global__ void __launch_bounds__(MF_THREADS)
     int* done = Q.done + (int64_t)b * ns;
     const double* Kb = Kval + b * nnzk;
     if (Q.task_big[task]) {
-      const int s = Q.task_sn[task * SMALL_WARPS];
+      const int s = Q.task_sn[Q.task_ptr[task]];
       const unsigned long long t0 = gtimer();
       if (threadIdx.x == 0)
         for (int ci = S.ch_ptr[s]; ci < S.ch_ptr[s + 1]; ++ci)
@@ -378,8 +381,16 @@ __global__ void __launch_bounds__(MF_THREADS)
       }
       if (threadIdx.x == 0) st_release(done + s, epoch);
     } else {
-      const int s = Q.task_sn[task * SMALL_WARPS + warp];
-      if (s >= 0) {
+      // a chunk of one-warp fronts of one level (no dependencies inside it): the warps pull fronts from
+      // a shared counter, so a warp that finishes early takes the next front instead of idling until the
+      // slowest warp of a fixed bundle is done (the arithmetic of a front does not depend on the warp)
+      const int q0 = Q.task_ptr[task], q1 = Q.task_ptr[task + 1];
+      for (;;) {
+        int q = 0;
+        if (lane == 0) q = q0 + atomicAdd(&chunk_ctr, 1);
+        q = __shfl_sync(0xffffffffu, q, 0);
+        if (q >= q1) break;
+        const int s = Q.task_sn[q];
         const unsigned long long t0 = gtimer();
         if (lane == 0)
           for (int ci = S.ch_ptr[s]; ci < S.ch_ptr[s + 1]; ++ci)
@@ -397,6 +408,8 @@ __global__ void __launch_bounds__(MF_THREADS)
         }
         if (lane == 0) st_release(done + s, epoch);
       }
+      __syncthreads();
+      if (threadIdx.x == 0) chunk_ctr = 0;  // (next_ticket's barrier orders this before the next chunk)
     }
   }
 }
