@@ -3,7 +3,8 @@
 The paper runs MadNLP's filter line-search interior-point method ([17] = Wächter and
 Biegler) with the condensed-KKT Newton step on the GPU.  This module is that loop for NLPs of the
 form  min f(v)  s.t.  c(v) = 0,  lo <= v_B <= hi  (bounds on a subset B of the variables),
-with the per-iteration linear algebra entirely in libckkt (HyKKT, m_e = m, m_i = 0):
+with the per-iteration linear algebra entirely in libckkt — HyKKT (GpuKKT: m_e = m, m_i = 0), or Lifted-KKT
+on the relaxed problem of P:333-346 (LiftedNLP + LiftedGpuKKT: m_e = 0, every row relaxed with a slack):
 
   * inertia correction: ckkt_refactor_inertia (reading R15, P:236-247, P:347-350);
   * Newton step: ckkt_solve of  [W + Sigma_x + delta_x I, J^T; J, 0] [dx; dlam] = -[r1; r3]  with
@@ -75,6 +76,85 @@ class GpuKKT:
         rc, info = self.ctx.solve(self._t(r1), None, self._t(r3), None, dx, None, dy, None)
         # CG / refinement non-convergence still returns the best iterate (include/ckkt.h); reported per step
         return dx.cpu().numpy(), dy.cpu().numpy(), dict(info[0], rc=int(rc))
+
+    def fraction_to_boundary(self, s, ds, tau):
+        a = self.ckkt.fraction_to_boundary(self._t(s), self._t(ds), tau)
+        return float(a.cpu().numpy()[0])
+
+
+class LiftedNLP:
+    """The relaxed problem of Lifted-KKT (Eq. problemrelaxation): min f(v) s.t. -tau <= c(v) <= tau
+    and the variable bounds, written with one slack per row as an NLP in w = (v, s):
+        min f(v)  s.t.  c(v) + s = 0,  lo <= v_B <= hi,  -tau <= s <= tau      (tau = 1e-6).
+    Its primal-dual Newton system [W + Sigma_v, 0, J^T; 0, Sigma_s, I; J, I, 0] is exactly the ABI's K_aug
+    of the Lifted strategy with H = J and D_s = Sigma_s (LiftedGpuKKT maps the calls), so solve_nlp
+    drives it unchanged: the slack rows of the gradient become r2, the constraint residual c + s becomes
+    r4, the multipliers of the relaxed rows are the ABI's dz."""
+
+    def __init__(self, nlp, tau=1e-6):
+        self.base, self.tau = nlp, tau
+        n, m = nlp.n, nlp.m
+        self.nv, self.m = n, m
+        self.n = n + m
+        self.pat = nlp.pat
+        self.bidx = np.concatenate([nlp.bidx, n + np.arange(m)])
+        self.lo = np.concatenate([nlp.lo, np.full(m, -tau)])
+        self.hi = np.concatenate([nlp.hi, np.full(m, tau)])
+        s0 = np.clip(-nlp.c(nlp.x0), -0.9 * tau, 0.9 * tau)  # feasible start: s = -c(x0) inside the box
+        self.x0 = np.concatenate([nlp.x0, s0])
+        self.lam0 = nlp.lam0.copy()
+
+    def f(self, w):
+        return self.base.f(w[:self.nv])
+
+    def grad_f(self, w):
+        return np.concatenate([self.base.grad_f(w[:self.nv]), np.zeros(self.m)])
+
+    def c(self, w):
+        return self.base.c(w[:self.nv]) + w[self.nv:]
+
+    def jac(self, w):  # values of J (the slack part of [J I] is the identity)
+        return self.base.jac(w[:self.nv])
+
+    def jac_t(self, w, jv, y):
+        return np.concatenate([self.base.jac_t(w[:self.nv], jv, y), y])
+
+    def hess(self, w, lam):  # W of the v block (f and c are linear in s)
+        return self.base.hess(w[:self.nv], lam)
+
+
+class LiftedGpuKKT:
+    """The per-iteration solve of LiftedNLP through libckkt with the Lifted-KKT strategy (m_e = 0, H = J,
+    D_s = Sigma_s): refactor(w, j, sigma_w, delta_last) -> (ok, delta, trials); solve(r1_w, c_w) ->
+    (dw, dlam, info)."""
+
+    def __init__(self, n, m, w_row, w_col, j_rowptr, j_col, leaf=64, device=0):
+        import torch
+        from . import ckkt
+        self.torch, self.ckkt = torch, ckkt
+        self.dev = torch.device("cuda", device)
+        self.n, self.m = n, m
+        self.ctx = ckkt.Context(n, 0, m, w_row, w_col, None, None, j_rowptr, j_col, strategy=ckkt.CKKT_LIFTED,
+                                leaf=leaf, device=device, stream=torch.cuda.current_stream(self.dev).cuda_stream)
+        self.delta = torch.zeros(1, dtype=torch.float64, device=self.dev)
+
+    def _t(self, a):
+        return self.torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64), device=self.dev)
+
+    def refactor(self, w_val, j_val, sigma_w, delta_last):
+        n = self.n
+        self._vals = [self._t(w_val), None, self._t(j_val), self._t(sigma_w[:n]), self._t(sigma_w[n:])]
+        rc, d, t = self.ctx.refactor_inertia(*self._vals, self.delta, np.array([delta_last]))
+        return rc == self.ckkt.CKKT_OK, float(d[0]), int(t[0])
+
+    def solve(self, r1_w, c_w):
+        T, n, m = self.torch, self.n, self.m
+        dx = T.empty(n, dtype=T.float64, device=self.dev)
+        ds = T.empty(m, dtype=T.float64, device=self.dev)
+        dz = T.empty(m, dtype=T.float64, device=self.dev)
+        rc, info = self.ctx.solve(self._t(r1_w[:n]), self._t(r1_w[n:]), None, self._t(c_w), dx, ds, None, dz)
+        dw = np.concatenate([dx.cpu().numpy(), ds.cpu().numpy()])
+        return dw, dz.cpu().numpy(), dict(info[0], rc=int(rc))
 
     def fraction_to_boundary(self, s, ds, tau):
         a = self.ckkt.fraction_to_boundary(self._t(s), self._t(ds), tau)
