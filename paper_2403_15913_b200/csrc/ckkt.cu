@@ -236,6 +236,7 @@ __global__ void k_gt_spmv(int n, int me, const int32_t* __restrict__ gt_ptr, con
   if (j >= n || (skip && skip[b])) return;
   const double* g = g_val + b * g_nnz;
   double acc = 0.0;
+  #pragma unroll 4
   for (int t = gt_ptr[j]; t < gt_ptr[j + 1]; ++t) acc += g[t] * v[(int64_t)b * me + gt_r[t]];
   double r = alpha * acc;
   if (z) r += beta * z[(int64_t)b * n + j];
@@ -252,6 +253,7 @@ __global__ void k_g_spmv(int me, int n, const int32_t* __restrict__ rowptr, cons
   if (r >= me || (skip && skip[b])) return;
   const double* g = g_val + b * g_nnz;
   double acc = 0.0;
+  #pragma unroll 4
   for (int e = rowptr[r]; e < rowptr[r + 1]; ++e) acc += g[e] * x[(int64_t)b * n + col2[e]];
   double res = alpha * acc;
   if (z) res += beta * z[(int64_t)b * me + r];
@@ -574,6 +576,7 @@ __device__ __forceinline__ void kaug_residual_row(const ResArgs& a, int b, int64
     const double* w = a.wsv + b * a.ws_nnz;
     const double* dx = a.dx + (int64_t)b * n;
     double acc = 0.0, aa = 0.0;
+    #pragma unroll 4
     for (int e = a.ws_ptr[i]; e < a.ws_ptr[i + 1]; ++e) {
       double v = w[e] * dx[a.ws_col[e]];
       acc += v;
@@ -584,6 +587,7 @@ __device__ __forceinline__ void kaug_residual_row(const ResArgs& a, int b, int64
     aa += fabs(dg);
     if (me) {
       const double* g = a.gtv + b * a.g_nnz;
+      #pragma unroll 4
       for (int e = a.gt_ptr[i]; e < a.gt_ptr[i + 1]; ++e) {
         double v = g[e] * a.dy[(int64_t)b * me + a.gt_r[e]];
         acc += v;
@@ -592,6 +596,7 @@ __device__ __forceinline__ void kaug_residual_row(const ResArgs& a, int b, int64
     }
     if (mi) {
       const double* h = a.htv + b * a.h_nnz;
+      #pragma unroll 4
       for (int e = a.ht_ptr[i]; e < a.ht_ptr[i + 1]; ++e) {
         double v = h[e] * a.dz[(int64_t)b * mi + a.ht_r[e]];
         acc += v;
@@ -614,6 +619,7 @@ __device__ __forceinline__ void kaug_residual_row(const ResArgs& a, int b, int64
     const double* g = a.g_val + b * a.g_nnz;
     const double* dx = a.dx + (int64_t)b * n;
     double acc = 0.0, aa = 0.0;
+    #pragma unroll 4
     for (int e = a.g_rowptr[r]; e < a.g_rowptr[r + 1]; ++e) {
       double v = g[e] * dx[a.g_col2[e]];
       acc += v;
@@ -628,6 +634,7 @@ __device__ __forceinline__ void kaug_residual_row(const ResArgs& a, int b, int64
     const double* h = a.h_val + b * a.h_nnz;
     const double* dx = a.dx + (int64_t)b * n;
     double acc = 0.0, aa = 0.0;
+    #pragma unroll 4
     for (int e = a.h_rowptr[r]; e < a.h_rowptr[r + 1]; ++e) {
       double v = h[e] * dx[a.h_col2[e]];
       acc += v;
