@@ -137,9 +137,11 @@ def build_inputs(N, instances, dev):
                                    device=dev)
     rh = [trajectory_rhs(n, m, i, T) for i in instances]
     rhs = lambda j: torch.as_tensor(np.stack([r[j] for r in rh], axis=1), device=dev)  # [T, B, len]
+    it0 = trajs[0][0]
     return {"pat": pat, "n": n, "m": m, "B": len(instances),
             "w": st("w_val"), "j": st("j_val"), "sig": st("sigma_x"), "dl": st("d_lifted"),
-            "r1": rhs(0), "ra": rhs(1), "rb": rhs(2)}
+            "r1": rhs(0), "ra": rhs(1), "rb": rhs(2),
+            "model": (insts[0].model, insts[0].xbar0, it0.v, it0.lam, insts[0].row_scale, insts[0].obj_scale)}
 
 
 def bench_config(args, world, n, m):
@@ -322,6 +324,31 @@ def run_ckkt(args, world, rank, local):
         d2h = 8 * B * (n + m)
         e2e = {"value": per_unit_ms(e_ms, args.steps, total_units), "unit": "ms/IPM-iter",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+    # NEXT-4: the model evaluation of one iterate (J, W, c, grad f) on the GPU (ckkt_distillation_eval) vs
+    # the numpy generator on the host (context: the paper's "AD" column)
+    md, xbar0, v0, lam0, rs0, sf0 = data["model"]
+    Td = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64), device=dev)
+    mv = [Td(xbar0), Td(v0), Td(lam0), Td(rs0)]
+    mo = [torch.empty(len(pat.j_col), dtype=torch.float64, device=dev),
+          torch.empty(len(pat.w_row), dtype=torch.float64, device=dev),
+          torch.empty(m, dtype=torch.float64, device=dev), torch.empty(n, dtype=torch.float64, device=dev)]
+    for _ in range(3):
+        ckkt.distillation_eval(N, md.p, mv[0], mv[1], mv[2], mv[3], sf0, *mo)
+    ev0.record(stream)
+    for _ in range(10):
+        ckkt.distillation_eval(N, md.p, mv[0], mv[1], mv[2], mv[3], sf0, *mo)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    me_gpu = ev0.elapsed_time(ev1) / 10
+    th = time.perf_counter()
+    md.jacobian_values(v0)
+    md.hessian_values(v0, lam0 * rs0, sf0)
+    md.residual(v0, xbar0)
+    md.grad_f(v0)
+    model_eval = {"gpu_ms": me_gpu, "host_numpy_ms": (time.perf_counter() - th) * 1e3,
+                  "outputs": "J, W (Lagrangian Hessian), c, grad f of one iterate",
+                  "bytes": 8 * (len(pat.j_col) + len(pat.w_row) + 2 * m + 2 * n)}
+    del mv, mo
     if rank != 0:
         if world > 1:
             torch.distributed.destroy_process_group()
@@ -405,6 +432,7 @@ def run_ckkt(args, world, rank, local):
         "roofline": roof,
         "factor_fp64": fp64,
         "e2e": e2e,
+        "model_eval": model_eval,
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "cpu_baseline": cpu,

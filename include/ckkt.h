@@ -227,6 +227,31 @@ ckkt_status ckkt_phase_times(ckkt_ctx *ctx, double *ms /* [CKKT_NPHASES] */, int
 /* Number of CUDA kernel launches enqueued by this context since creation (telemetry). */
 int64_t ckkt_launch_count(const ckkt_ctx *ctx);
 
+/* Model evaluation on the GPU (P:418-430 evaluates the model derivatives on the GPU
+ * with ExaModels): the distillation-column NLP of P:489-530 (reading A of DESIGN.md R12, gradient scaling
+ * R14), one warp per stage.  For `batch` instances (batch-major arrays, all DEVICE FP64):
+ *   v [B, 67(N+1)] the primal point (stage-major x_1..x_32, y_1..y_32, u, L, V);
+ *   lam [B, 66(N+1)] the equality multipliers (NULL = 0), row_scale [B, 66(N+1)] (NULL = 1), obj_scale;
+ *   xbar0 [32] the initial state (needed for c);
+ * out (any may be NULL): j_val [B, 288N+100] = row_scale * dg/dv in the CSR order of the pattern
+ * (inputs/distillation.build_pattern: rows stage-major, columns increasing), w_val [B, 96N+32] = the
+ * lower triangle of obj_scale grad^2 f + sum_r lam_r row_scale_r grad^2 g_r in the pattern's (row, col)
+ * order, c [B, 66(N+1)] = row_scale * g(v), grad_f [B, 67(N+1)] = obj_scale grad f(v).
+ * Asynchronous on `stream`; CKKT_INVALID_ARG for N < 1, batch < 1, a missing v / params, a feed tray
+ * outside 2..31, non-positive holdups or horizon. */
+typedef struct {
+  double alpha, D, F;      /* relative volatility, distillate and feed flows */
+  double w_x, rho;         /* objective weights on (x_1 - xbar_1)^2 and (u - ubar)^2 (w_x renamed, R12) */
+  double horizon;          /* dt = horizon / N */
+  double x_f, xbar1, ubar; /* feed composition, setpoints (unstated in the paper: SURVEY C14 fills) */
+  int32_t feed_tray;       /* 1-based feed tray */
+  double M[32];            /* tray holdups (C14: M_1 = M_32 = 5, else 1) */
+} ckkt_distillation_params;
+ckkt_status ckkt_distillation_eval(int32_t N, int32_t batch, const ckkt_distillation_params *params,
+                                   const double *xbar0, const double *v, const double *lam, const double *row_scale,
+                                   double obj_scale, double *j_val, double *w_val, double *c, double *grad_f,
+                                   void *stream);
+
 void ckkt_destroy(ckkt_ctx *ctx);
 const char *ckkt_status_str(ckkt_status s);
 

@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 LIB = os.path.join(HERE, "libckkt.so")
-SOURCES = ["analysis.cpp", "ckkt.cu"]
+SOURCES = ["analysis.cpp", "ckkt.cu", "model_eval.cu"]
 HEADERS = ["analysis.h", "mf_kernels.cuh", "dense_front.cuh", os.path.join(INCLUDE, "ckkt.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

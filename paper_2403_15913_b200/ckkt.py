@@ -23,7 +23,7 @@ EXPORTED = ["ckkt_default_options", "ckkt_setup", "ckkt_get_sizes", "ckkt_export
             "ckkt_export_elimination_order", "ckkt_export_analysis", "ckkt_setup_from_analysis", "ckkt_refactor",
             "ckkt_refactor_inertia", "ckkt_fraction_to_boundary",
             "ckkt_solve", "ckkt_iterate_host", "ckkt_profile", "ckkt_phase_times", "ckkt_launch_count",
-            "ckkt_destroy", "ckkt_status_str"]
+            "ckkt_destroy", "ckkt_status_str", "ckkt_distillation_eval"]
 PHASES = ("condense", "factor", "forward", "backward", "vector")
 
 
@@ -48,6 +48,13 @@ class ckkt_info(ctypes.Structure):
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class ckkt_distillation_params(ctypes.Structure):
+    _fields_ = [("alpha", ctypes.c_double), ("D", ctypes.c_double), ("F", ctypes.c_double),
+                ("w_x", ctypes.c_double), ("rho", ctypes.c_double), ("horizon", ctypes.c_double),
+                ("x_f", ctypes.c_double), ("xbar1", ctypes.c_double), ("ubar", ctypes.c_double),
+                ("feed_tray", ctypes.c_int32), ("M", ctypes.c_double * 32)]
 
 
 class ckkt_sizes(ctypes.Structure):
@@ -104,6 +111,9 @@ def lib():
         L.ckkt_launch_count.restype = ctypes.c_int64
         L.ckkt_destroy.argtypes = [P]
         L.ckkt_destroy.restype = None
+        L.ckkt_distillation_eval.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ckkt_distillation_params),
+                                             P, P, P, P, ctypes.c_double, P, P, P, P, P]
+        L.ckkt_distillation_eval.restype = ctypes.c_int
         L.ckkt_status_str.argtypes = [ctypes.c_int]
         L.ckkt_status_str.restype = ctypes.c_char_p
         _lib = L
@@ -125,6 +135,29 @@ def fraction_to_boundary(s, ds, tau: float):
     if rc:
         raise CKKTError(rc, "ckkt_fraction_to_boundary")
     return alpha
+
+
+def distillation_params(p) -> ckkt_distillation_params:
+    """ckkt_distillation_params from an inputs.distillation.Params-like object (attribute names match)."""
+    out = ckkt_distillation_params()
+    for name in ("alpha", "D", "F", "w_x", "rho", "horizon", "x_f", "xbar1", "ubar", "feed_tray"):
+        setattr(out, name, getattr(p, name))
+    for k, mk in enumerate(p.holdups()):
+        out.M[k] = float(mk)
+    return out
+
+
+def distillation_eval(N, params, xbar0, v, lam=None, row_scale=None, obj_scale=1.0, j_val=None, w_val=None, c=None,
+                      grad_f=None, batch=1):
+    """ckkt_distillation_eval on device tensors (outputs preallocated by the caller; any may be None), enqueued
+    on torch's current stream."""
+    import torch
+    prm = distillation_params(params)
+    rc = lib().ckkt_distillation_eval(int(N), int(batch), ctypes.byref(prm), _dptr(xbar0), _dptr(v), _dptr(lam),
+                                      _dptr(row_scale), float(obj_scale), _dptr(j_val), _dptr(w_val), _dptr(c),
+                                      _dptr(grad_f), ctypes.c_void_p(torch.cuda.current_stream(v.device).cuda_stream))
+    if rc:
+        raise CKKTError(rc, "ckkt_distillation_eval")
 
 
 class CKKTError(RuntimeError):
