@@ -344,7 +344,12 @@ __device__ void factor_big(const SymDev& S, int s, int b, double* Ps, double* ds
   if (ph) ph[6] = gtimer();
 }
 
-__global__ void __launch_bounds__(MF_THREADS)
+#ifdef CKKT_MF_MINB  // (experiments: force more resident CTAs per SM)
+#define CKKT_MF_BOUNDS __launch_bounds__(MF_THREADS, CKKT_MF_MINB)
+#else
+#define CKKT_MF_BOUNDS __launch_bounds__(MF_THREADS)
+#endif
+__global__ void CKKT_MF_BOUNDS
     k_factor_persist(SymDev S, Sched Q, int ns, int B, int epoch, double* L, int64_t Lsize, double* Ub,
                      int64_t Usize, const double* __restrict__ Kval, int64_t nnzk, int* notpd, int* minpiv,
                      const int8_t* __restrict__ tiny) {
