@@ -80,9 +80,11 @@ __global__ void k_condense(int64_t nnzk, const IDX* __restrict__ wt_ptr, const i
   const double* g = g_val + b * g_nnz;
   const double* h = h_val + b * h_nnz;
   double acc = 0.0;
+#pragma unroll 4
   for (IDX t = wt_ptr[k]; t < wt_ptr[k + 1]; ++t) acc += w[wt_idx[t]];
   const int dv = kdiag[k];
   if (dv >= 0) acc += sigma[(int64_t)b * n + dv] + (delta ? delta[b] : 0.0);
+#pragma unroll 4
   for (IDX t = jt_ptr[k]; t < jt_ptr[k + 1]; ++t) {
     if (MODE == 1) {
       acc += gamma * (g[jt_a[t]] * g[jt_b[t]]);
