@@ -264,7 +264,7 @@ def run_ckkt(args, world, rank, local):
     # phase split for the roofline: a second timed pass of the same steps with CUDA events around every
     # condense / factor / forward / backward / vector launch group (event brackets cannot live inside the
     # CG graph, so this pass runs the host-driven CG loop; kernel durations are the same)
-    prof_steps = min(args.steps, 3)
+    prof_steps = args.steps  # the same trajectory positions as the timed steps (their n_ref / k_cg differ)
     ctx.profile(True)
     for k in range(prof_steps):
         step((args.warmup + k) % T)
@@ -383,7 +383,7 @@ def run_ckkt(args, world, rank, local):
 
     dom = max((k for k in phases if k in algo), key=lambda k: phases[k][0])
     roof = roof_entry(dom)
-    roof["phase_pass"] = ("CUDA events on the library stream per launch group, separate pass of min(steps, 3) "
+    roof["phase_pass"] = ("CUDA events on the library stream per launch group, separate pass of the same "
                           "steps of the same workload (host-driven CG loop)")
     roof["phases_ms_per_step"] = {k: v[0] / args.steps for k, v in phases.items()}
     roof["launches_per_step"] = {k: v[1] / args.steps for k, v in phases.items()}
