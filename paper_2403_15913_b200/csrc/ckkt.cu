@@ -961,7 +961,7 @@ ckkt_status setup_device(ckkt_ctx* c) {
           tbig.push_back(1);
           tsn.push_back(s);
           tptr.push_back((int32_t)tsn.size());
-          const int64_t mp = (m + 7) & ~7, wp = (w + 3) & ~3;
+          const int64_t mp = big_ldp((int)m), wp = (w + 3) & ~3;
           c->big_smem = std::max<int64_t>(c->big_smem, 8 * (mp * wp + 8));
         }
       }

@@ -230,30 +230,62 @@ __device__ __forceinline__ void extend_add(const double* __restrict__ Uc, int mc
 // U = -L21 L21^T (mu x mu, lower, column-major) from the panel in shared memory (ld ldp, L21 at row
 // offset w), on 8x8 DMMA tiles (mma.sync.m8n8k4.f64); warps take tiles round robin.  Rows >= mu and
 // columns >= w read as zero (guards), so the arithmetic is the same for padded and unpadded panels.
+__device__ __forceinline__ void upd_tile_ij(int tI, int& I, int& J) {
+  I = (int)((sqrt(8.0 * tI + 1.0) - 1.0) * 0.5);
+  while ((I + 1) * (I + 2) / 2 <= tI) ++I;
+  while (I * (I + 1) / 2 > tI) --I;
+  J = tI - I * (I + 1) / 2;
+}
+
+#ifndef CKKT_UPD_TU
+#define CKKT_UPD_TU 1
+#endif
+#ifndef CKKT_UPD_UNROLL
+#define CKKT_UPD_UNROLL 2
+#endif
+constexpr int UPD_UNROLL = CKKT_UPD_UNROLL;
+// A warp computes CKKT_UPD_TU tiles at a time (tiles tI, tI + nwarp, ...; independent DMMA chains in
+// one k loop) with the k loop unrolled CKKT_UPD_UNROLL times, so the next fragments load while the
+// current DMMA runs.  Each tile's k order is fixed (results do not depend on either knob).  Measured
+// at C3 (factor): TU 1 / unroll 2 12.47 ms, TU 2 12.65, TU 4 12.79 (spills), unroll 4 12.69,
+// unroll 8 13.26, no unroll 12.81.
 __device__ __forceinline__ void front_update_dmma(const double* Ps, int ldp, int w, int mu, int lane, int warp,
                                                   int nwarp, double* U) {
+  constexpr int TU = CKKT_UPD_TU;
   const int nb = (mu + 7) >> 3;
   const int ntile = nb * (nb + 1) / 2;
   const int g = lane >> 2, t4 = lane & 3;
-  for (int tI = warp; tI < ntile; tI += nwarp) {
-    int I = (int)((sqrt(8.0 * tI + 1.0) - 1.0) * 0.5);
-    while ((I + 1) * (I + 2) / 2 <= tI) ++I;
-    while (I * (I + 1) / 2 > tI) --I;
-    const int J = tI - I * (I + 1) / 2;
-    double c0 = 0.0, c1 = 0.0;
-    const int ia = I * 8 + g, ib = J * 8 + g;
-    const double* ra = Ps + w + ia;
-    const double* rb = Ps + w + ib;
+  for (int t0 = warp; t0 < ntile; t0 += TU * nwarp) {
+    int ia[TU], ib[TU];
+    double c0[TU], c1[TU];
+#pragma unroll
+    for (int u = 0; u < TU; ++u) {
+      const int tI = t0 + u * nwarp;
+      int I = 0, J = 0;
+      if (tI < ntile) upd_tile_ij(tI, I, J);
+      ia[u] = (tI < ntile) ? I * 8 + g : mu;  // rows >= mu read as zero
+      ib[u] = (tI < ntile) ? J * 8 + g : mu;
+      c0[u] = c1[u] = 0.0;
+    }
+#pragma unroll UPD_UNROLL
     for (int k = 0; k < w; k += 4) {
       const int kk = k + t4;
-      const double a = (ia < mu && kk < w) ? ra[kk * ldp] : 0.0;
-      const double b = (ib < mu && kk < w) ? rb[kk * ldp] : 0.0;
-      dmma_8x8x4(c0, c1, a, b);
+#pragma unroll
+      for (int u = 0; u < TU; ++u) {
+        const double a = (ia[u] < mu && kk < w) ? Ps[w + ia[u] + kk * ldp] : 0.0;
+        const double b = (ib[u] < mu && kk < w) ? Ps[w + ib[u] + kk * ldp] : 0.0;
+        dmma_8x8x4(c0[u], c1[u], a, b);
+      }
     }
-    const int row = I * 8 + g, col = J * 8 + 2 * t4;
-    if (row < mu) {
-      if (col < mu) U[row + (int64_t)col * mu] = -c0;
-      if (col + 1 < mu) U[row + (int64_t)(col + 1) * mu] = -c1;
+#pragma unroll
+    for (int u = 0; u < TU; ++u) {
+      const int tI = t0 + u * nwarp;
+      if (tI >= ntile) continue;
+      const int row = ia[u], col = ib[u] - g + 2 * t4;
+      if (row < mu) {
+        if (col < mu) U[row + (int64_t)col * mu] = -c0[u];
+        if (col + 1 < mu) U[row + (int64_t)(col + 1) * mu] = -c1[u];
+      }
     }
   }
 }
@@ -297,7 +329,19 @@ __device__ void factor_small(const SymDev& S, int s, int b, int tid, double* Ps,
   }
 }
 
-// big supernode, whole CTA, panel in shared memory with ld = mp (m padded to 8, w padded to 4)
+// Leading dimension of a CTA front's shared-memory panel: m rounded up to 8 doubles and then to
+// 8 mod 16, so that the DMMA fragment loads (lanes g + 8 t4 ... rows g, columns t4) fall into 16
+// distinct double-banks twice each — two wavefronts per 32-lane load, the minimum; a multiple of
+// 16 would put all four column groups on the same 8 banks (four wavefronts).
+__host__ __device__ constexpr int big_ldp(int m) {
+#ifdef CKKT_NO_LDP_PAD
+  return (m + 7) & ~7;
+#else
+  return (((m + 7) & ~7) & 15) ? ((m + 7) & ~7) : ((m + 7) & ~7) + 8;
+#endif
+}
+
+// big supernode, whole CTA, panel in shared memory with ld = mp = big_ldp(m) (m padded to 8, w padded to 4)
 __device__ void factor_big(const SymDev& S, int s, int b, double* Ps, double* dsh, double* L, int64_t Lsize,
                            double* Ub, int64_t Usize, const double* __restrict__ Kb, int* notpd, int* minpiv) {
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -305,7 +349,7 @@ __device__ void factor_big(const SymDev& S, int s, int b, double* Ps, double* ds
   const int f = S.sfirst[s], w = S.sfirst[s + 1] - f;
   const int m = (int)(S.srowptr[s + 1] - S.srowptr[s]);
   const int mu = m - w;
-  const int mp = (m + 7) & ~7, wp = (w + 3) & ~3, ldp = mp;
+  const int mp = big_ldp(m), wp = (w + 3) & ~3, ldp = mp;
   double* P = L + b * Lsize + S.pofs[s];
   double* U = Ub + b * Usize + S.uofs[s];
   CKB(S.pofs[s] + (int64_t)m * w <= Lsize && S.uofs[s] + (int64_t)mu * mu <= Usize && w <= 64);
@@ -429,7 +473,7 @@ constexpr int SOLVE_WARPS = 8;
 #define CKKT_SOLVE_MINB 3
 #endif
 constexpr int SOLVE_MINB = CKKT_SOLVE_MINB;  // resident CTAs per SM the register budget is sized for
-constexpr int TOP_PANEL = 4096;  // panels above this (doubles) and their ancestors go to the top set
+constexpr int TOP_PANEL = 5120;  // panels above this (doubles) and their ancestors go to the top set
 // Bottom-set sweeps run one supernode per WORKER of LW lanes (a warp, or a half warp: two
 // independent supernode chains interleaved in one warp hide more memory latency per SM).
 #ifndef CKKT_LW
