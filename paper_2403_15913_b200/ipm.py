@@ -19,12 +19,15 @@ on the relaxed problem of P:333-346 (LiftedNLP + LiftedGpuKKT: m_e = 0, every ro
     E_mu <= 10 mu; stop when E_0 <= tol (tol = 1e-6).
 
 Host arithmetic here is O(n) vector bookkeeping in numpy on iterates copied back from the device;
-the model evaluation (f, c, J, W) is the caller's `problem` (ExaModels AD is out of scope, §8(f) 4).
+the model evaluation (f, c, J, W) is the caller's `problem`: the host model (inputs.distillation.NLP) or
+DeviceDistillationNLP, whose J and W come from the GPU kernel ckkt_distillation_eval (NEXT-4) and go to
+the KKT solve without leaving the device (general AD as in ExaModels is out of scope, §8(f) 4).
 """
 from __future__ import annotations
 
 import dataclasses
 import math
+import warnings
 
 import numpy as np
 
@@ -62,6 +65,8 @@ class GpuKKT:
         self.delta = torch.zeros(1, dtype=torch.float64, device=self.dev)
 
     def _t(self, a):
+        if isinstance(a, self.torch.Tensor):  # device values (DeviceDistillationNLP): no host round trip
+            return a.to(device=self.dev, dtype=self.torch.float64).contiguous()
         return self.torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64), device=self.dev)
 
     def refactor(self, w_val, j_val, sigma_x, delta_last):
@@ -80,6 +85,75 @@ class GpuKKT:
     def fraction_to_boundary(self, s, ds, tau):
         a = self.ckkt.fraction_to_boundary(self._t(s), self._t(ds), tau)
         return float(a.cpu().numpy()[0])
+
+
+def transpose_pattern(j_rowptr, j_col, n):
+    """CSR pattern of J^T from J's (rowptr, col): (ptr [n+1], col [nnz] = J's row of each entry, perm [nnz])
+    with values_T = values_J[perm] (entries of a J column in increasing row order)."""
+    j_rowptr, j_col = np.asarray(j_rowptr), np.asarray(j_col)
+    rows = np.repeat(np.arange(j_rowptr.size - 1), np.diff(j_rowptr))
+    perm = np.lexsort((rows, j_col))
+    ptr = np.concatenate([[0], np.cumsum(np.bincount(j_col, minlength=n))])
+    return ptr, rows[perm], perm
+
+
+class DeviceDistillationNLP:
+    """The distillation NLP with its derivatives evaluated on the GPU (the
+    paper evaluates the model with ExaModels on the device, so J and W never cross to the host).  Same
+    callbacks as the host model `base` (inputs.distillation.NLP), except that jac / hess return device
+    tensors from ckkt_distillation_eval, which GpuKKT / LiftedGpuKKT hand to libckkt without a copy; c and
+    grad_f are evaluated on the device and copied back (O(n) vectors for the line search); J^T y is a
+    device CSR product of the transposed pattern (host-driver bookkeeping, not the hot path); f stays the
+    host objective of `base`."""
+
+    def __init__(self, base, device=0):
+        import torch
+        from . import ckkt
+        inst = base.inst
+        self.base, self.torch, self.ckkt = base, torch, ckkt
+        self.dev = torch.device("cuda", device)
+        self.N, self.params = base.md.N, base.md.p
+        self.n, self.m, self.pat = base.n, base.m, base.pat
+        self.bidx, self.lo, self.hi = base.bidx, base.lo, base.hi
+        self.x0, self.lam0 = base.x0.copy(), base.lam0.copy()
+        T = lambda a, dt=torch.float64: torch.as_tensor(np.ascontiguousarray(a), dtype=dt, device=self.dev)
+        self._T = T
+        self._xbar0, self._rs, self._sf = T(inst.xbar0), T(inst.row_scale), float(inst.obj_scale)
+        t_ptr, t_col, perm = transpose_pattern(self.pat.j_rowptr, self.pat.j_col, self.n)
+        self._t_ptr, self._t_col, self._t_perm = (T(a, torch.int64) for a in (t_ptr, t_col, perm))
+
+    def _eval(self, v, lam=None, j=False, w=False, c=False, g=False):
+        torch = self.torch
+        e = lambda k: torch.empty(k, dtype=torch.float64, device=self.dev)
+        out = dict(j=e(self.pat.j_col.size) if j else None, w=e(self.pat.w_row.size) if w else None,
+                   c=e(self.m) if c else None, g=e(self.n) if g else None)
+        self.ckkt.distillation_eval(self.N, self.params, self._xbar0, self._T(v), None if lam is None else self._T(lam),
+                                    self._rs, self._sf, out["j"], out["w"], out["c"], out["g"])
+        return out
+
+    def f(self, v):
+        return self.base.f(v)
+
+    def grad_f(self, v):
+        return self._eval(v, g=True)["g"].cpu().numpy()
+
+    def c(self, v):
+        return self._eval(v, c=True)["c"].cpu().numpy()
+
+    def jac(self, v):
+        return self._eval(v, j=True)["j"]
+
+    def jac_t(self, v, jv, y):
+        torch = self.torch
+        vals = self._T(jv) if not isinstance(jv, torch.Tensor) else jv
+        with warnings.catch_warnings():  # (torch's "sparse CSR is beta" notice)
+            warnings.simplefilter("ignore", UserWarning)
+            jt = torch.sparse_csr_tensor(self._t_ptr, self._t_col, vals[self._t_perm], size=(self.n, self.m),
+                                         check_invariants=False)
+            return (jt @ self._T(y)).cpu().numpy()
+
+    def hess(self, v, lam):
+        return self._eval(v, lam=lam, w=True)["w"]
 
 
 class LiftedNLP:
@@ -139,6 +213,8 @@ class LiftedGpuKKT:
         self.delta = torch.zeros(1, dtype=torch.float64, device=self.dev)
 
     def _t(self, a):
+        if isinstance(a, self.torch.Tensor):  # device values (DeviceDistillationNLP): no host round trip
+            return a.to(device=self.dev, dtype=self.torch.float64).contiguous()
         return self.torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64), device=self.dev)
 
     def refactor(self, w_val, j_val, sigma_w, delta_last):

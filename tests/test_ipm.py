@@ -194,3 +194,53 @@ def test_ipm_gpu_lifted_iteration_parity():
     _check_lifted(lg, r_g)
     assert r_g.iterations == r_o.iterations
     assert abs(r_g.objective - r_o.objective) <= 1e-8 * max(1.0, abs(r_o.objective))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("lifted", [False, True])
+def test_ipm_gpu_device_model(lifted):
+    """NEXT-4 inside NEXT-1: the IPM with the model derivatives evaluated on the GPU
+    (ipm.DeviceDistillationNLP: J and W from ckkt_distillation_eval go to libckkt without a host round
+    trip) takes the same iterations to the same optimum as with the host model, for HyKKT and for
+    Lifted-KKT on the relaxed problem (N = 10)."""
+    def run(device_model):
+        base = dist.NLP(dist.Instance(10))
+        nlp = ipm.DeviceDistillationNLP(base) if device_model else base
+        if lifted:
+            nlp = ipm.LiftedNLP(nlp)
+            p = nlp.pat
+            kkt = ipm.LiftedGpuKKT(nlp.nv, nlp.m, p.w_row, p.w_col, p.j_rowptr, p.j_col)
+        else:
+            p = nlp.pat
+            kkt = ipm.GpuKKT(nlp.n, nlp.m, p.w_row, p.w_col, p.j_rowptr, p.j_col)
+        return nlp, ipm.solve_nlp(nlp, kkt, max_iter=200)
+    nh, rh = run(False)
+    nd, rd = run(True)
+    if lifted:
+        _check_lifted(nh, rh)
+        _check_lifted(nd, rd)
+    else:
+        _check_solution(nh, rh)
+        _check_solution(nd.base, rd)
+    assert rd.iterations == rh.iterations
+    assert abs(rd.objective - rh.objective) <= 1e-8 * max(1.0, abs(rh.objective))
+    # both runs stop at the IPM tolerance 1e-6 (P:590); the relaxed problem's slacks / duals are less
+    # well determined, so its iterates agree to O(tol) rather than better
+    assert np.abs(rd.v - rh.v).max() <= (1e-5 if lifted else 1e-6)
+
+
+def test_transpose_pattern_matches_scipy():
+    """The J^T pattern DeviceDistillationNLP multiplies with (host logic, no GPU): values gathered through
+    perm reproduce scipy's transpose of the distillation Jacobian pattern."""
+    from scipy.sparse import csr_matrix
+    pat = dist.build_pattern(7)
+    rng = np.random.default_rng(5)
+    jv = rng.standard_normal(pat.j_col.size)
+    ptr, col, perm = ipm.transpose_pattern(pat.j_rowptr, pat.j_col, pat.n)
+    ref = csr_matrix((jv, pat.j_col, pat.j_rowptr), shape=(pat.m, pat.n)).T.tocsr()
+    ref.sort_indices()
+    assert np.array_equal(ptr, ref.indptr) and np.array_equal(col, ref.indices)
+    assert np.array_equal(jv[perm], ref.data)
+    y = rng.standard_normal(pat.m)
+    got = np.array([jv[perm][ptr[i]:ptr[i + 1]] @ y[col[ptr[i]:ptr[i + 1]]] for i in range(pat.n)])
+    assert np.allclose(got, ref @ y, rtol=1e-14, atol=1e-14)
