@@ -3,8 +3,10 @@ consecutive kernels, the largest gap classes by (previous kernel -> next kernel)
 time.  Explains the "other" share of bench.py's phase split (step time not covered by kernel work).
 Usage: python tools/timeline.py [config] [steps]"""
 import collections
+import json
 import os
 import sys
+import tempfile
 
 import torch
 
@@ -43,14 +45,17 @@ with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) a
     ev1.record(stream)
     torch.cuda.synchronize()
 wall = ev0.elapsed_time(ev1) * 1e3  # us
-evs = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
-ks = sorted(((e.time_range.start, e.time_range.end, e.name or getattr(e, "key", "")) for e in evs), key=lambda t: t[0])
+# kernel / memcpy / memset records from the chrome trace (names included for kernels launched by libckkt)
+with tempfile.NamedTemporaryFile(suffix=".json") as tf:
+    prof.export_chrome_trace(tf.name)
+    trace = json.load(open(tf.name))
+ks = sorted(((float(e["ts"]), float(e["ts"]) + float(e.get("dur", 0.0)), e.get("name", ""))
+             for e in trace.get("traceEvents", [])
+             if e.get("ph") == "X" and e.get("cat") in ("kernel", "gpu_memcpy", "gpu_memset")), key=lambda t: t[0])
 busy, gaps, prev_end, prev_name = 0.0, collections.Counter(), None, None
 gapn = collections.Counter()
 per = collections.Counter()
 cnt = collections.Counter()
-if ks and not any(t[2] for t in ks):  # kernel names missing on this build: report the key averages instead
-    print(prof.key_averages().table(sort_by="self_device_time_total", row_limit=40))
 for s, e, name in ks:
     short = name.split("(")[0].replace("void ", "").replace("(anonymous namespace)::", "").replace("<unnamed>::", "")
     per[short] += e - s
