@@ -207,7 +207,9 @@ ckkt_status ckkt_solve(ckkt_ctx *ctx, const double *r1, const double *r2, const 
 
 /* End-to-end iteration from HOST buffers (pinned recommended): copies the values and
  * right-hand sides to the device, refactorizes, solves and copies the step back.
- * Same array shapes as ckkt_refactor / ckkt_solve, all host pointers. Synchronous. */
+ * Same array shapes as ckkt_refactor / ckkt_solve, all host pointers. Synchronous.
+ * The right-hand sides travel on a context-owned second stream after the values, while the
+ * factorization runs (overlap needs pinned buffers; pageable ones are copied synchronously). */
 ckkt_status ckkt_iterate_host(ckkt_ctx *ctx, const double *w_val, const double *g_val, const double *h_val,
                               const double *sigma_x, const double *d_s, const double *delta_x,
                               const double *r1, const double *r2, const double *r3, const double *r4,

@@ -829,6 +829,9 @@ struct ckkt_ctx {
   double *st_r1 = nullptr, *st_r2 = nullptr, *st_r3 = nullptr, *st_r4 = nullptr;
   double *st_dx = nullptr, *st_ds_o = nullptr, *st_dy = nullptr, *st_dz = nullptr;
   int* st_notpd = nullptr;
+  // ckkt_iterate_host: the right-hand sides are copied on a second stream while the refactorization runs
+  cudaStream_t st_aux = nullptr;
+  cudaEvent_t ev_vals = nullptr, ev_rhs = nullptr;
 };
 
 namespace {
@@ -1307,6 +1310,9 @@ ckkt_status setup_device(ckkt_ctx* c) {
   DALLOC(c->st_dy, Bme);
   DALLOC(c->st_dz, Bmi);
   DALLOC(c->st_notpd, B);
+  CK(cudaStreamCreateWithFlags(&c->st_aux, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&c->ev_vals, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->ev_rhs, cudaEventDisableTiming));
   // the CG loop graph is captured here too (it reads only context-owned memory)
   if (me > 0 && c->stream != nullptr && !sync_debug() && !getenv("CKKT_NO_GRAPH")) {
     if (!build_cg_graph(c)) {
@@ -1365,6 +1371,9 @@ void ckkt_destroy(ckkt_ctx* c) {
     }
     if (c->cg_exec) cudaGraphExecDestroy(c->cg_exec);
     if (c->cg_graph) cudaGraphDestroy(c->cg_graph);
+    if (c->ev_vals) cudaEventDestroy(c->ev_vals);
+    if (c->ev_rhs) cudaEventDestroy(c->ev_rhs);
+    if (c->st_aux) cudaStreamDestroy(c->st_aux);
     for (void* p : c->owned) cudaFree(p);
     if (c->h_pinned_int) cudaFreeHost(c->h_pinned_int);
     if (c->h_pinned_dbl) cudaFreeHost(c->h_pinned_dbl);
@@ -2116,23 +2125,33 @@ extern "C" ckkt_status ckkt_iterate_host(ckkt_ctx* c, const double* w_val, const
   const int B = c->B;
   const size_t Bn = (size_t)B * c->n, Bme = (size_t)B * c->me, Bmi = (size_t)B * c->mi;
   cudaStream_t st = c->stream;
-  auto h2d = [&](double* dst, const double* src, size_t cnt) -> cudaError_t {
+  auto h2d = [&](double* dst, const double* src, size_t cnt, cudaStream_t sx) -> cudaError_t {
     if (!src || cnt == 0) return cudaSuccess;
-    return cudaMemcpyAsync(dst, src, sizeof(double) * cnt, cudaMemcpyHostToDevice, st);
+    return cudaMemcpyAsync(dst, src, sizeof(double) * cnt, cudaMemcpyHostToDevice, sx);
   };
-  CK(h2d(c->st_w, w_val, (size_t)B * c->w_nnz));
-  CK(h2d(c->st_g, g_val, (size_t)B * c->g_nnz));
-  CK(h2d(c->st_h, h_val, (size_t)B * c->h_nnz));
-  CK(h2d(c->st_sig, sigma_x, Bn));
-  CK(h2d(c->st_ds, d_s, Bmi));
-  CK(h2d(c->st_del, delta_x, B));
-  CK(h2d(c->st_r1, r1, Bn));
-  CK(h2d(c->st_r2, r2, Bmi));
-  CK(h2d(c->st_r3, r3, Bme));
-  CK(h2d(c->st_r4, r4, Bmi));
+  // the matrix values first (the refactorization needs them), then the right-hand sides on the
+  // auxiliary stream, after the values (one link), overlapping the factorization; the solve waits
+  // for them.  (The previous call ended with a stream synchronisation, so the staging is free.)
+  CK(h2d(c->st_w, w_val, (size_t)B * c->w_nnz, st));
+  CK(h2d(c->st_g, g_val, (size_t)B * c->g_nnz, st));
+  CK(h2d(c->st_h, h_val, (size_t)B * c->h_nnz, st));
+  CK(h2d(c->st_sig, sigma_x, Bn, st));
+  CK(h2d(c->st_ds, d_s, Bmi, st));
+  CK(h2d(c->st_del, delta_x, B, st));
+  CK(cudaEventRecord(c->ev_vals, st));
+  CK(cudaStreamWaitEvent(c->st_aux, c->ev_vals, 0));
+  CK(h2d(c->st_r1, r1, Bn, c->st_aux));
+  CK(h2d(c->st_r2, r2, Bmi, c->st_aux));
+  CK(h2d(c->st_r3, r3, Bme, c->st_aux));
+  CK(h2d(c->st_r4, r4, Bmi, c->st_aux));
+  CK(cudaEventRecord(c->ev_rhs, c->st_aux));
   ckkt_status s = ckkt_refactor(c, c->st_w, c->st_g, c->st_h, c->st_sig, c->st_ds, delta_x ? c->st_del : nullptr,
                                 c->st_notpd, nullptr);
-  if (s != CKKT_OK) return s;
+  CK(cudaStreamWaitEvent(st, c->ev_rhs, 0));
+  if (s != CKKT_OK) {
+    CK(cudaStreamSynchronize(st));
+    return s;
+  }
   std::vector<ckkt_info> tmp(B);
   s = ckkt_solve(c, c->st_r1, c->st_r2, c->st_r3, c->st_r4, c->st_dx, c->st_ds_o, c->st_dy, c->st_dz,
                  info ? info : tmp.data());

@@ -258,3 +258,28 @@ def test_front_paths_bit_identical(strategy, monkeypatch):
         g = run_gpu(case, strategy, leaf=268)
         for name in ("dx", "ds", "dy", "dz"):
             assert np.array_equal(g[name].view(np.int64), ref[name].view(np.int64)), (panel, name)
+
+
+@pytest.mark.parametrize("strategy", [1, 0])
+def test_iterate_host_matches_device_calls(strategy):
+    """ckkt_iterate_host (values and right-hand sides from pinned HOST buffers, the right-hand sides on the
+    context's second stream during the factorization) returns bit-for-bit the step and info of
+    ckkt_refactor + ckkt_solve on device buffers, on a batch of two distillation iterates, twice in a row
+    (the staging buffers are reused)."""
+    import torch
+    case = distillation_case(50, strategy, iterates=[2, 11])
+    g = run_gpu(case, strategy, leaf=64)
+    ctx, B = g["ctx"], case.B
+    P = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64)).pin_memory() if a.size else None
+    E = lambda k: torch.empty((B, k), dtype=torch.float64).pin_memory() if k else None
+    hv = [P(case.w_val), P(case.g_val), P(case.h_val), P(case.sigma_x), P(case.d_s), P(case.delta_x)]
+    hr = [P(case.r1), P(case.r2), P(case.r3), P(case.r4)]
+    for _ in range(2):
+        out = [E(case.n), E(case.m_i), E(case.m_e), E(case.m_i)]
+        rc, info = ctx.iterate_host(*hv, *hr, *out)
+        assert rc == g["rc"]
+        for name, t in zip(("dx", "ds", "dy", "dz"), out):
+            if t is not None:
+                assert np.array_equal(t.numpy(), g[name]), name
+        for b in range(B):
+            assert info[b] == g["info"][b]
