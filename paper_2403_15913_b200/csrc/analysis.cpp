@@ -585,8 +585,6 @@ std::string analyze(const Pattern& p, int leaf, const int32_t* user_perm, Analys
   for (int k = 0; k < n; ++k) A.iperm2[A.perm2[k]] = k;
 
   // ---- internal symbolic
-  std::vector<int64_t> Lp2;
-  std::vector<int32_t> Li2;
   {
     std::vector<int64_t> rp;
     std::vector<int32_t> rc;
@@ -597,7 +595,7 @@ std::string analyze(const Pattern& p, int leaf, const int32_t* user_perm, Analys
     for (int k = 0; k < n; ++k) ipost[post[k]] = k;
     A.parent2.resize(n);
     for (int k = 0; k < n; ++k) A.parent2[k] = A.parent[post[k]] < 0 ? -1 : ipost[A.parent[post[k]]];
-    row_subtrees(n, rp, rc, A.parent2, A.colcount2, &Lp2, &Li2);
+    row_subtrees(n, rp, rc, A.parent2, A.colcount2, nullptr, nullptr);  // column counts only
     A.colcount.resize(n);
     for (int k = 0; k < n; ++k) A.colcount[post[k]] = A.colcount2[k];
     A.nnz_l = 0;
@@ -691,17 +689,50 @@ std::string analyze(const Pattern& p, int leaf, const int32_t* user_perm, Analys
       A.srowptr[s2 + 1] = A.srowptr[s2] + m;
       A.pofs[s2 + 1] = A.pofs[s2] + m * w;
     }
+    // Row structures of the group tops, by a postorder merge over the fundamental-supernode tree
+    // (only a fundamental supernode's first column has children outside it):
+    //   below(F) = rows > last(F) of K's columns in F and of below(C) for the children C of F,
+    // checked against the column counts of the row-subtree pass; the L column of first(F) is then
+    // first(F)..last(F) followed by below(F).  Work and memory ~ sum of the structures, not nnz(L).
+    std::vector<std::vector<int32_t>> below(nf);
+    {
+      std::vector<char> need(nf, 0);
+      for (int s2 = 0; s2 < A.ns; ++s2) need[stopf[s2]] = 1;
+      std::vector<int32_t> chead(nf, -1), cnext(nf, -1);
+      for (int F = nf - 1; F >= 0; --F)
+        if (fsparent[F] >= 0) { cnext[F] = chead[fsparent[F]]; chead[fsparent[F]] = F; }
+      std::vector<int32_t> buf, mark(n, -1);  // mark[i] == F: row i already collected for F
+      for (int F = 0; F < nf; ++F) {
+        const int f0 = fsfirst[F], l = fsfirst[F + 1] - 1;
+        buf.clear();
+        auto add = [&](int32_t i) {
+          if (i > l && mark[i] != F) {
+            mark[i] = F;
+            buf.push_back(i);
+          }
+        };
+        for (int j = f0; j <= l; ++j)
+          for (int64_t q = A.kp[j]; q < A.kp[j + 1]; ++q) add(A.ki[q]);
+        for (int C = chead[F]; C >= 0; C = cnext[C]) {
+          for (int32_t i : below[C]) add(i);
+          if (!need[C]) std::vector<int32_t>().swap(below[C]);
+        }
+        std::sort(buf.begin(), buf.end());
+        if ((int64_t)buf.size() != (int64_t)A.colcount2[f0] - (l - f0 + 1)) {
+          code = CKKT_INVALID_ARG;
+          return "internal error: supernodal structure disagrees with the column counts";
+        }
+        below[F] = buf;
+      }
+    }
     A.srows.resize(A.srowptr[A.ns]);
     for (int s2 = 0; s2 < A.ns; ++s2) {
       const int top = stopf[s2];
       int64_t o = A.srowptr[s2];
-      for (int j = A.sfirst[s2]; j < fsfirst[top]; ++j) A.srows[o++] = j;
-      if (A.sfirst[s2] <= fsfirst[top]) {
-        std::copy(Li2.begin() + Lp2[fsfirst[top]], Li2.begin() + Lp2[fsfirst[top] + 1], A.srows.begin() + o);
-      } else {  // chunk starting inside the top fundamental supernode: suffix of its structure
-        const int skip = A.sfirst[s2] - fsfirst[top];
-        std::copy(Li2.begin() + Lp2[fsfirst[top]] + skip, Li2.begin() + Lp2[fsfirst[top] + 1], A.srows.begin() + o);
-      }
+      // columns sfirst[s2] .. last(top) (a chunk may start inside the top fundamental supernode),
+      // then the structure below the top
+      for (int j = A.sfirst[s2]; j < fsfirst[top + 1]; ++j) A.srows[o++] = j;
+      std::copy(below[top].begin(), below[top].end(), A.srows.begin() + o);
     }
     A.sparent.assign(A.ns, -1);
     for (int s2 = 0; s2 < A.ns; ++s2) {
@@ -710,8 +741,6 @@ std::string analyze(const Pattern& p, int leaf, const int32_t* user_perm, Analys
     }
   }
   const int ns = A.ns;
-  Li2.clear();
-  Li2.shrink_to_fit();
   // levels (children before parents; postorder => child index < parent index)
   A.slevel.assign(ns, 0);
   for (int s = 0; s < ns; ++s)
