@@ -369,8 +369,9 @@ def run_ckkt(args, world, rank, local):
              "backward": "k_bwd_top + k_bwd_persist + k_bwd_tiny (one backward sweep)",
              "factor": "k_factor_tiny + k_factor_persist (one numeric factorization)",
              "condense": "k_condense"}
+    # DRAM bytes per launch from the committed ncu capture, which is of the default workload (C3) only
     tr_path = os.path.join(ROOT, "profiles", "traffic.json")
-    traffic = json.load(open(tr_path)) if os.path.exists(tr_path) else {}
+    traffic = json.load(open(tr_path)) if os.path.exists(tr_path) and args.config == "c3" else {}
 
     def roof_entry(ph):
         ms_tot, cnt = phases[ph]

@@ -39,3 +39,27 @@ def test_gpus_flag_spawns_ranks():
     assert len(lines) == 1
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["config"]["parallelism"].startswith("replicas x2")
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.gpu
+def test_gpu_arm_json_line():
+    """The GPU arm on the small config: one JSON line with the contract's keys, the roofline / CPU
+    baseline / e2e / clocks objects and a positive count of the library's own kernel launches."""
+    lines = _run(["--config", "c1", "--steps", "3", "--warmup", "3"])
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert (KEYS - {"impl"}) <= set(d), KEYS - set(d)
+    assert d["dtype"] == "f64" and d["higher_is_better"] is False and d["value"] > 0 and d["n_gpus"] == 1
+    r = d["roofline"]
+    assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(r)
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1 and r["achieved"] > 0
+    assert r["traffic"] is None  # the committed ncu capture is of C3, not of this config
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) <= 1e-9 * r["frac"]
+    e = d["e2e"]
+    assert e["value"] >= d["value"] * 0.5 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] > 0
+    assert d["gpu_launches"] > 0
+    assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
