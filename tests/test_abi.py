@@ -209,3 +209,54 @@ def test_parallel_analysis_matches_oracle_and_thread_count(N, leaf, monkeypatch)
     o = OK.SparseKKT(pat.n, pat.m, 0, pat.w_row, pat.w_col, pat.j_rowptr, pat.j_col, E32, E32[:0], leaf=leaf)
     assert np.array_equal(perm, o.perm) and np.array_equal(parent, o.parent) and np.array_equal(cc, o.colcount)
     assert np.array_equal(Lp, o.Lp) and np.array_equal(Li, o.Li)
+
+
+def _debug_get(ctx, what, dt):
+    L = ckkt.lib()
+    L.ckkt_debug_get.restype = ctypes.c_int64
+    L.ckkt_debug_get.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
+    cnt = L.ckkt_debug_get(ctx.h, what, None)
+    a = np.empty(cnt, dt)
+    L.ckkt_debug_get(ctx.h, what, a.ctypes.data_as(ctypes.c_void_p))
+    return a
+
+
+@pytest.mark.parametrize("case", ["dist3", "dist40", "rand0", "rand1", "rand2", "rand3"])
+def test_supernode_row_structures_cover_the_factor(case):
+    """The supernodes' row lists (built by a postorder merge over the fundamental-supernode tree, not
+    from the L pattern) against the exact L pattern of the internal order, obtained from the exported
+    (oracle-pinned) symbolic relabelled by the postorder: every supernode lists its own columns first,
+    rows ascending and unique, and contains the L structure of each of its columns (amalgamated
+    supernodes may hold more rows: their explicit zeros)."""
+    if case.startswith("dist"):
+        pat = dist.build_pattern(int(case[4:]))
+        ctx = _host_ctx(pat.n, pat.m, 0, pat.w_row, pat.w_col, pat.j_rowptr, pat.j_col, None, None, leaf=64)
+        n = pat.n
+    else:
+        seed = int(case[4:])
+        rng = np.random.default_rng(100 + seed)
+        n = int(rng.integers(20, 120))
+        me, mi = int(rng.integers(0, n // 2)), int(rng.integers(0, n))
+        inst = random_instance(n, me, mi, seed=seed, density=float(rng.uniform(0.03, 0.15)))
+        ctx = _host_ctx(n, me, mi, inst.w_row, inst.w_col, inst.g_rowptr, inst.g_col, inst.h_rowptr, inst.h_col,
+                        leaf=int(rng.integers(2, 20)))
+    perm, parent, cc, Lp, Li = ctx.export_symbolic()
+    perm2 = _debug_get(ctx, 2, np.int32)
+    sfirst = _debug_get(ctx, 3, np.int32)
+    srp = _debug_get(ctx, 4, np.int64)
+    srows = _debug_get(ctx, 5, np.int32)
+    iperm = np.empty(n, np.int64)
+    iperm[perm] = np.arange(n)
+    post = iperm[perm2]                 # internal column k = exported column post[k]
+    ipost = np.empty(n, np.int64)
+    ipost[post] = np.arange(n)
+    for s in range(sfirst.size - 1):
+        f, l = int(sfirst[s]), int(sfirst[s + 1])
+        rows = srows[srp[s]:srp[s + 1]]
+        assert np.array_equal(rows[:l - f], np.arange(f, l))
+        assert np.all(np.diff(rows) > 0)
+        have = set(rows.tolist())
+        for k in range(f, l):
+            j = post[k]
+            struct = ipost[Li[Lp[j]:Lp[j + 1]]]
+            assert struct.min() == k and set(struct.tolist()) <= have, (s, k)
