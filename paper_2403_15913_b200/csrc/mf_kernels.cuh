@@ -635,6 +635,46 @@ __device__ __forceinline__ void warp_gather_children(const SymDev& S, const Swee
       if (!cm.tiny) wait_epoch(done + cm.c, A.epoch);
     }
     wsync();
+#ifndef CKKT_GATHER_SERIAL
+    // the first 2 LW rows of GK children at a time: all their loads in flight together (one round
+    // trip instead of one per child), then applied child by child in order (deterministic); rows
+    // beyond 2 LW (rare) follow for each child right after its first rows
+#ifndef CKKT_GK
+#define CKKT_GK 4
+#endif
+    constexpr int GK = CKKT_GK;
+    for (int k0 = 0; k0 < nc; k0 += GK) {
+      double uv[GK][2];
+      int rl[GK][2];
+#pragma unroll
+      for (int kk = 0; kk < GK; ++kk) {
+        const int k = k0 + kk;
+        const int mc = (k < nc) ? cmeta[k].mc : 0;
+        const double* uc = Vb + ((k < nc) ? cmeta[k].vofs : 0);
+        const int32_t* rel = S.relmap + ((k < nc) ? cmeta[k].relofs : 0);
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int i = lane + r * LW;
+          rl[kk][r] = (i < mc) ? __ldg(rel + i) : -1;
+          uv[kk][r] = (i < mc) ? __ldcg(uc + i) : 0.0;
+        }
+      }
+#pragma unroll
+      for (int kk = 0; kk < GK; ++kk) {
+        const int k = k0 + kk;
+        if (k >= nc) break;
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+          if (rl[kk][r] >= 0) {
+            CKB(rl[kk][r] < M.m && cmeta[k].vofs + cmeta[k].mc <= A.Vsize);
+            v[rl[kk][r]] += uv[kk][r];
+          }
+        const ChMeta& cm = cmeta[k];
+        for (int i = 2 * LW + lane; i < cm.mc; i += LW) v[__ldg(S.relmap + cm.relofs + i)] += __ldcg(Vb + cm.vofs + i);
+        wsync();
+      }
+    }
+#else
     for (int k = 0; k < nc; ++k) {
       const ChMeta cm = cmeta[k];
       const double* uc = Vb + cm.vofs;
@@ -646,6 +686,7 @@ __device__ __forceinline__ void warp_gather_children(const SymDev& S, const Swee
       }
       wsync();
     }
+#endif
   }
 }
 
