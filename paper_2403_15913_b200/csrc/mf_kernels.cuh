@@ -482,7 +482,7 @@ constexpr int TOP_PANEL = 5120;  // panels above this (doubles) and their ancest
 constexpr int LW = CKKT_LW;
 constexpr int SOLVE_WORKERS = 32 * SOLVE_WARPS / LW;  // workers per CTA
 constexpr int RED_LD = LW + 1;                         // column stride of the per-worker reduction scratch
-constexpr int RED_SZ = 16 * RED_LD;                    // doubles of it (16 columns per batch)
+constexpr int RED_SZ = 16 * RED_LD + 32;               // doubles of it (16 columns per batch + stage 2)
 static_assert(LW == 32 || LW == 16, "worker width");
 
 __device__ __forceinline__ unsigned worker_mask() {
@@ -567,12 +567,36 @@ __device__ __forceinline__ void warp_coldot_rb(const double* __restrict__ A, int
 #pragma unroll
     for (int cc = 0; cc < CB; ++cc) red[cc * RED_LD + lane] = acc[cc];
     wsync();
+#ifndef CKKT_COLDOT_SERIAL
+    {  // two stages with every lane busy: lane (j, h) sums segment h (CB partials) of column j, then
+       // lane j < CB adds its column's H segment sums (CB + H dependent adds instead of LW)
+      constexpr int H = LW / CB;
+      const int j = lane % CB, h = lane / CB;
+      const double* q = red + j * RED_LD + h * CB;
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < CB; k += 2) {
+        s0 += q[k];
+        s1 += q[k + 1];
+      }
+      red[16 * RED_LD + j * H + h] = s0 + s1;
+    }
+    wsync();
+    if (lane < CB && c0 + lane < ncols) {
+      constexpr int H = LW / CB;
+      double v = 0.0;
+#pragma unroll
+      for (int h = 0; h < H; ++h) v += red[16 * RED_LD + lane * H + h];
+      out[c0 + lane] = (init ? init[c0 + lane] : 0.0) + sgn * v;
+    }
+#else
     if (lane < CB && c0 + lane < ncols) {
       double v = 0.0;
 #pragma unroll 8
       for (int l = 0; l < LW; ++l) v += red[lane * RED_LD + l];
       out[c0 + lane] = (init ? init[c0 + lane] : 0.0) + sgn * v;
     }
+#endif
     wsync();
   }
 }
