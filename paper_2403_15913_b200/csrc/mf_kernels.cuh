@@ -1242,8 +1242,21 @@ __global__ void __launch_bounds__(256)
       for (int i = g; i < cm.mc; i += TG) v[__ldg(rel + i)] += __ldcg(uc + i);
       __syncwarp(mask);
     }
-    // y = Z v[0:w] (every lane of the group, broadcast loads); lane k < w stores y_k
     double y[TINY_W];
+#ifndef CKKT_TINY_Y_ALL
+    // y = Z v[0:w]: lane k < w computes y_k, the group shares them by shuffles
+    {
+      static_assert(TINY_W <= TG, "one lane per column of a tiny supernode");
+      double yk = 0.0;
+#pragma unroll
+      for (int j = 0; j < TINY_W; ++j)
+        if (j <= g && g < w) yk += P[g + j * m] * v[j];
+      const int lane0 = (threadIdx.x & 31) & ~(TG - 1);
+#pragma unroll
+      for (int k = 0; k < TINY_W; ++k) y[k] = __shfl_sync(mask, yk, lane0 + k);
+    }
+#else
+    // y = Z v[0:w] (every lane of the group, broadcast loads); lane k < w stores y_k
 #pragma unroll
     for (int k = 0; k < TINY_W; ++k) {
       double acc = 0.0;
@@ -1252,6 +1265,7 @@ __global__ void __launch_bounds__(256)
         if (j <= k && k < w) acc += P[k + j * m] * v[j];
       y[k] = acc;
     }
+#endif
 #pragma unroll
     for (int k = 0; k < TINY_W; ++k)
       if (k % TG == g && k < w) x[f + k] = y[k];
@@ -1305,10 +1319,20 @@ __global__ void __launch_bounds__(256)
           if (c < w) part[c] -= P[i + c * m] * xi;
       }
     }
+    double tv[TINY_W];
+#ifndef CKKT_TINY_RED_SMEM
+    // butterfly over the group's TG lanes (every lane ends with every column's sum)
+#pragma unroll
+    for (int c = 0; c < TINY_W; ++c) {
+      double v = part[c];
+#pragma unroll
+      for (int o = TG / 2; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o);
+      tv[c] = ((c < w) ? x[f + c] : 0.0) + v;
+    }
+#else
 #pragma unroll
     for (int c = 0; c < TINY_W; ++c) red[c][g] = part[c];
     __syncwarp(mask);
-    double tv[TINY_W];
 #pragma unroll
     for (int c = 0; c < TINY_W; ++c) {
       double acc = (c < w) ? x[f + c] : 0.0;
@@ -1316,6 +1340,7 @@ __global__ void __launch_bounds__(256)
       for (int l = 0; l < TG; ++l) acc += red[c][l];
       tv[c] = acc;
     }
+#endif
     // x_s = Z^T t: lane i < w computes row i
 #pragma unroll
     for (int i = 0; i < TINY_W; ++i) {
