@@ -716,14 +716,25 @@ __device__ __forceinline__ void warp_gather_children(const SymDev& S, const Swee
 
 // forward step of supernode s by one worker (v, y: per-worker shared scratch)
 __device__ __forceinline__ void fwd_warp_step(const SymDev& S, const SweepArgs& A, const SnMeta& M, int s, int b,
-                                              int lane, double* v, double* y, ChMeta* cmeta, int* done) {
+                                              int lane, double* v, double* y, ChMeta* cmeta, int* done,
+                                              int rel_prev) {
   double* x = A.X + (int64_t)b * A.n;
   const int f = M.f, w = M.w, m = M.m, mu = m - w;
   const double* P = A.L + b * A.Lsize + M.pofs;
   CKB(M.pofs + (int64_t)m * w <= A.Lsize && M.vofs + mu <= A.Vsize && f + w <= A.n && m <= A.max_m);
   if (lane == 0) prefetch_l2(P, 8ll * m * w);  // the panel streams into L2 while the children are gathered
   const unsigned long long t0 = g_debug_ts ? gtimer() : 0ull;
-  for (int i = lane; i < m; i += LW) v[i] = (i < w) ? x[f + i] : 0.0;
+  // this step's x loads are issued before the previous step's flag is published (deferred release,
+  // before any wait of this step): the release fence then overlaps the loads' round trip
+  constexpr int XR = 64 / LW;  // w <= 64
+  double xw[XR];
+#pragma unroll
+  for (int r = 0; r < XR; ++r) xw[r] = (lane + r * LW < w) ? x[f + lane + r * LW] : 0.0;
+  if (rel_prev >= 0 && lane == 0) st_release(done + rel_prev, A.epoch);
+#pragma unroll
+  for (int r = 0; r < XR; ++r)
+    if (lane + r * LW < m) v[lane + r * LW] = xw[r];
+  for (int i = lane + 64; i < m; i += LW) v[i] = 0.0;
   warp_gather_children(S, A, M, b, lane, v, cmeta, done);
   warp_gemv(P, m, w, w, v, nullptr, 1.0, y, lane);  // y = Z v[0:w]  (Z strict upper part is zero)
   wsync();
@@ -780,28 +791,41 @@ __global__ void __launch_bounds__(32 * SOLVE_WARPS, SOLVE_MINB) k_fwd_persist(Sy
     const bool sk = A.skip && A.skip[b];
     const int q0 = A.chunk_ptr[ch], n = A.chunk_ptr[ch + 1] - q0;
     if (!sk) warp_stage_chunk(S, A, q0, n, b, lane, msh, false);
+    int pend = -1;  // supernode whose flag is published at the start of the next step of the chunk
     for (int j = 0; j < n; ++j) {
       const int s = sk ? A.queue[q0 + j] : msh[j].pad1;
       if (!sk) {
-        fwd_warp_step(S, A, msh[j], s, b, lane, v, y, cmeta, done);
+        fwd_warp_step(S, A, msh[j], s, b, lane, v, y, cmeta, done, pend);
         wsync();
+        pend = s;
+      } else if (lane == 0) {
+        st_release(done + s, A.epoch);
       }
-      if (lane == 0) st_release(done + s, A.epoch);
     }
+    if (pend >= 0 && lane == 0) st_release(done + pend, A.epoch);
     wsync();
   }
 }
 
 // backward step of supernode s by one worker: x_s = Z^T (y_s - L21^T x_R)
 __device__ __forceinline__ void bwd_warp_step(const SymDev& S, const SweepArgs& A, const SnMeta& M, int s, int b,
-                                              int lane, double* xr, double* tv, double* red, int* ridx, int* done) {
+                                              int lane, double* xr, double* tv, double* red, int* ridx, int* done,
+                                              int rel_prev) {
   const int p = M.pad0;
   double* x = A.X + (int64_t)b * A.n;
   const int f = M.f, w = M.w, m = M.m, mu = m - w;
   const double* P = A.L + b * A.Lsize + M.pofs;
   CKB(M.pofs + (int64_t)m * w <= A.Lsize && f + w <= A.n && m <= A.max_m);
   if (lane == 0) prefetch_l2(P, 8ll * m * w);  // independent of the parent: overlap with the wait
-  for (int i = lane; i < w; i += LW) tv[i] = x[f + i];
+  constexpr int XR = 64 / LW;  // w <= 64
+  double xw[XR];
+#pragma unroll
+  for (int r = 0; r < XR; ++r) xw[r] = (lane + r * LW < w) ? x[f + lane + r * LW] : 0.0;
+  // the previous step's flag is published after this step's first loads are issued (see fwd)
+  if (rel_prev >= 0 && lane == 0) st_release(done + rel_prev, A.epoch);
+#pragma unroll
+  for (int r = 0; r < XR; ++r)
+    if (lane + r * LW < w) tv[lane + r * LW] = xw[r];
   for (int i = lane; i < mu; i += LW) {
     ridx[i] = __ldg(S.srows + M.r0 + w + i);
     CKB(ridx[i] >= f + w && ridx[i] < A.n);
@@ -849,14 +873,18 @@ __global__ void __launch_bounds__(32 * SOLVE_WARPS, SOLVE_MINB) k_bwd_persist(Sy
     const bool sk = A.skip && A.skip[b];
     const int q0 = A.chunk_ptr[ch], n = A.chunk_ptr[ch + 1] - q0;
     if (!sk) warp_stage_chunk(S, A, q0, n, b, lane, msh, true);
+    int pend = -1;
     for (int j = n - 1; j >= 0; --j) {
       const int s = sk ? A.queue[q0 + j] : msh[j].pad1;
       if (!sk) {
-        bwd_warp_step(S, A, msh[j], s, b, lane, xr, tv, red, ridx, done);
+        bwd_warp_step(S, A, msh[j], s, b, lane, xr, tv, red, ridx, done, pend);
         wsync();
+        pend = s;
+      } else if (lane == 0) {
+        st_release(done + s, A.epoch);
       }
-      if (lane == 0) st_release(done + s, A.epoch);
     }
+    if (pend >= 0 && lane == 0) st_release(done + pend, A.epoch);
     wsync();
   }
 }
