@@ -1316,13 +1316,17 @@ __global__ void __launch_bounds__(256)
 __global__ void __launch_bounds__(256)
     k_bwd_tiny(SymDev S, const SnMeta* __restrict__ tmeta, const int32_t* __restrict__ sub_ptr, int nsub, int B,
                const double* __restrict__ L, int64_t Lsize, double* X, int n, const int* __restrict__ skip) {
+#ifdef CKKT_TINY_RED_SMEM
   __shared__ double red_all[256 / TG][TINY_W][TG + 1];
+#endif
   const int gid = (blockIdx.x * blockDim.x + threadIdx.x) / TG, g = threadIdx.x % TG;
   if (gid >= nsub * B) return;
   const unsigned mask = (TG == 32 ? 0xFFFFFFFFu : ((1u << TG) - 1u)) << ((threadIdx.x & 31) & ~(TG - 1));
   const int sub = gid / B, b = gid % B;
   if (skip && skip[b]) return;
+#ifdef CKKT_TINY_RED_SMEM
   auto red = red_all[threadIdx.x / TG];
+#endif
   double* x = X + (int64_t)b * n;
   const int q0 = sub_ptr[sub];
   if (g == 0) {  // contiguous span of the subtree's panels
