@@ -11,6 +11,7 @@
 //   a9 flags             NOT_PD / minimum failing pivot
 // All n-vectors on the device live in the internal elimination order (perm2).
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX 3: host ranges for nsys timelines (no-ops without a tool)
 
 #include <algorithm>
 #include <array>
@@ -51,6 +52,12 @@ static bool sync_debug() {
       if (e_ != cudaSuccess) fprintf(stderr, "ckkt: kernel %s failed: %s\n", name, cudaGetErrorString(e_)); \
     }                                                                                           \
   } while (0)
+
+// NVTX range over one ABI call (SURVEY §5 tracing: the phases show up by name in an nsys timeline)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 namespace {
 
@@ -1409,6 +1416,7 @@ ckkt_status ckkt_export_analysis(const ckkt_ctx* c, void* buf, int64_t* size) {
 
 static ckkt_status setup_impl(const ckkt_pattern* p, const ckkt_options* opt, const void* blob, int64_t blob_size,
                               ckkt_ctx** out) {
+  NvtxRange nvtx_range("ckkt_setup");
   if (!p || !out) return CKKT_INVALID_ARG;
   *out = nullptr;
   ckkt_options o;
@@ -1553,6 +1561,7 @@ ckkt_status ckkt_phase_times(ckkt_ctx* c, double* ms, int64_t* count) {
 ckkt_status ckkt_refactor(ckkt_ctx* c, const double* w_val, const double* g_val, const double* h_val,
                           const double* sigma_x, const double* d_s, const double* delta_x, int32_t* not_pd,
                           int32_t* min_bad_pivot) {
+  NvtxRange nvtx_range("ckkt_refactor");
   if (!c || !c->has_device) return CKKT_INVALID_ARG;
   if ((c->w_nnz && !w_val) || !sigma_x || (c->g_nnz && !g_val) || (c->h_nnz && !h_val) || (c->mi && !d_s))
     return CKKT_INVALID_ARG;
@@ -1642,6 +1651,7 @@ ckkt_status ckkt_refactor(ckkt_ctx* c, const double* w_val, const double* g_val,
 ckkt_status ckkt_refactor_inertia(ckkt_ctx* c, const double* w_val, const double* g_val, const double* h_val,
                                   const double* sigma_x, const double* d_s, const double* delta_last,
                                   double* delta_x, double* delta_out, int32_t* trials_out, int32_t* not_pd) {
+  NvtxRange nvtx_range("ckkt_refactor_inertia");
   if (!c || !c->has_device || !delta_x) return CKKT_INVALID_ARG;
   const int B = c->B;
   cudaStream_t st = c->stream;
@@ -1990,6 +2000,7 @@ void residual(ckkt_ctx* c, const double* r1, const double* r2, const double* r3,
 
 extern "C" ckkt_status ckkt_solve(ckkt_ctx* c, const double* r1, const double* r2, const double* r3, const double* r4,
                                   double* dx, double* ds, double* dy, double* dz, ckkt_info* info) {
+  NvtxRange nvtx_range("ckkt_solve");
   if (!c || !c->has_device || !c->factored) return CKKT_INVALID_ARG;
   const int n = c->n, me = c->me, mi = c->mi, B = c->B;
   if (!r1 || !dx || (me && (!r3 || !dy)) || (mi && (!r2 || !r4 || !ds || !dz))) return CKKT_INVALID_ARG;
@@ -2120,6 +2131,7 @@ extern "C" ckkt_status ckkt_iterate_host(ckkt_ctx* c, const double* w_val, const
                                          const double* r1, const double* r2, const double* r3, const double* r4,
                                          double* dx, double* ds, double* dy, double* dz, int32_t* not_pd,
                                          ckkt_info* info) {
+  NvtxRange nvtx_range("ckkt_iterate_host");
   if (!c || !c->has_device) return CKKT_INVALID_ARG;
   CK(cudaSetDevice(c->opt.device));
   const int B = c->B;
