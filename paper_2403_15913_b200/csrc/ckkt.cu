@@ -1145,6 +1145,8 @@ ckkt_status setup_device(ckkt_ctx* c) {
         const int64_t fcap = (per_cta - (int64_t)fa.sharedSizeBytes) / 8 - (c->max_m + 64);
         const int64_t bcap = (per_cta - (int64_t)ba.sharedSizeBytes) / 8 - (c->max_m + 128);
         c->topbuf = (int)std::max<int64_t>(0, std::min<int64_t>(maxp + 2, std::min(fcap, bcap)) & ~int64_t(1));
+        if (const char* e = getenv("CKKT_TOPBUF"))  // experiments: cap the staging buffer (0 = panels from L2)
+          c->topbuf = std::min(c->topbuf, std::max(0, atoi(e)) & ~1);
         c->ftop_smem = 8 * ((int64_t)c->topbuf + c->max_m + 64);
         c->btop_smem = 8 * ((int64_t)c->topbuf + c->max_m + 128);
         CK(cudaFuncSetAttribute(k_fwd_top, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->ftop_smem));
