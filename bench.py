@@ -406,7 +406,11 @@ def run_ckkt(args, world, rank, local):
                     "rel_res_unrefined_max": float(max(i["rel_res_unrefined"] for i in infos)),
                     "n_ref_mean": float(np.mean([i["n_ref"] for i in infos])),
                     "rel_res_max": float(max(i["rel_res"] for i in infos)),
-                    "status_max": int(max(i["status"] for i in infos))}
+                    "status_max": int(max(i["status"] for i in infos)),
+                    # per timed step (instance 0): correction passes and CG iterations, the work that
+                    # moves the step time besides the kernels
+                    "n_ref_per_step": [int(i["n_ref"]) for i in infos[::B]],
+                    "k_cg_total_per_step": [int(i["k_cg_total"]) for i in infos[::B]]}
     out = {
         "metric": "KKT refactor+solve ms/IPM-iter (FP64)",
         "value": per_unit_ms(ms, args.steps, total_units),
