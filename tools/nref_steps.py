@@ -1,3 +1,6 @@
+"""Per trajectory position of bench.py's timed steps (C3, HyKKT): first-pass CG iterations, total CG
+iterations, correction passes and the unrefined / refined omega -- shows which iterates need a second
+correction pass.  Usage: [TAG=label] python tools/nref_steps.py"""
 import os, sys
 sys.path.insert(0, '/root/repo')
 import torch, numpy as np
