@@ -2,7 +2,7 @@
 iterations, correction passes and the unrefined / refined omega -- shows which iterates need a second
 correction pass.  Usage: [TAG=label] python tools/nref_steps.py"""
 import os, sys
-sys.path.insert(0, '/root/repo')
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, numpy as np
 import bench
 from paper_2403_15913_b200 import ckkt
